@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""qdot B200 benchmark (driver contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1]): qdot of two
+standard-normal fp64 vectors of n = 2^28 per GPU (default_rng(0), x then y),
+epsilon = 1e-8, SplitMode.NONE, ExactBinning.  At N > 1 every rank holds its
+own 2^28-element shard of one N*2^28-element dot product (C5 at N = 8) and
+the ranks exchange the exponent histogram and the exact per-key partial sums
+over NCCL (weak scaling).  A "step" is one full qdot: begin + pass1 +
+allreduce(A) + score + pass2 + allreduce(B) + finalize.
+
+`value` = elements/s with inputs resident in HBM (CUDA events, max over
+ranks); `e2e` = the same metric through the public API qdot() from pinned
+host memory (H2D of x, y and the D2H of the result inside the timed region).
+Inputs (4 GiB per GPU) are far larger than the 126 MB L2, so no L2 flush is
+needed between steps.
+
+--impl reference times the CPU oracle port (oracle/qdot_oracle.c, the C
+restatement of the reference path; the reference itself is Python and is
+not installable on the GPU box) on a bounded sample with all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "qdot elements/s and HBM GB/s (% of roofline) at n=2^28 fp64, 1/2/4/8 B200"
+N_PER_GPU = 1 << 28
+EPS = 1e-8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--norm", action="store_true", help="norm mode x.x (8 B/elem)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profile_traffic():
+    """dram bytes per pass1 launch from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "pass1_ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("n")
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_baseline(n_sample: int, steps: int = 1):
+    """Oracle port (C restatement of the reference path), all host threads."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    x, y = O.gen_normal(n_sample, seed=0)
+    O.qdot(x[:4096], y[:4096], EPS)  # warm
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        O.qdot(x, y, EPS)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": n_sample / best, "unit": "elements/s", "cores": threads, "kind": "port",
+            "sample": f"qdot n={n_sample} standard-normal eps=1e-8 exact, oracle/qdot_oracle.c, "
+                      f"best of {len(times)}"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    steps = max(1, args.steps if args.steps <= 5 else 3)
+    warm = min(args.warmup, 1)
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    n_s = args.cpu_sample
+    x, y = O.gen_normal(n_s, seed=0)
+    for _ in range(warm):
+        O.qdot(x, y, EPS)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.qdot(x, y, EPS)
+    dt = (time.perf_counter() - t0) / steps
+    val = n_s / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "elements/s", "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 qdot fp64 standard-normal eps=1e-8 exact (bounded CPU sample)",
+                   "n_sample": n_s, "threads": threads},
+        "cpu_baseline": {"value": val, "unit": "elements/s", "cores": threads, "kind": "port",
+                         "sample": f"n={n_s} per step (of the 2^28 workload)"},
+        "e2e": {"value": val, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import ctypes
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2105_00115_b200 as Q
+    from paper_2105_00115_b200 import _lib
+    from paper_2105_00115_b200.device import config_struct, thread_state
+    lib = _lib.load()
+
+    n = args.n
+    # synthetic inputs: rank r draws its shard with default_rng(r) (rank 0 == the C2 golden input)
+    rng = np.random.default_rng(rank)
+    xh = rng.standard_normal(n)
+    yh = xh if args.norm else rng.standard_normal(n)
+    xd = torch.from_numpy(xh).to(dev)
+    yd = xd if args.norm else torch.from_numpy(yh).to(dev)
+    cfg = Q.ToleranceConfig(EPS)
+    c = config_struct(cfg, Q.ExactBinning())
+    st = thread_state(dev)
+    stream = torch.cuda.current_stream(dev)
+    s = stream.cuda_stream
+    ws = st.ws_ptr
+    norm = int(args.norm)
+    xp, yp = xd.data_ptr(), yd.data_ptr()
+    n_total = n * world
+    ra, rb = st.region_a(), st.region_b()
+    ev_p1 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)]
+
+    def step(i=None):
+        _lib.check(lib.qdot_b200_begin(ws, s), lib)
+        if i is not None:
+            ev_p1[i][0].record(stream)
+        _lib.check(lib.qdot_b200_pass1(xp, yp, n, norm, ws, s), lib)
+        if i is not None:
+            ev_p1[i][1].record(stream)
+        if world > 1:
+            torch.distributed.all_reduce(ra)
+        _lib.check(lib.qdot_b200_score(ws, n_total, ctypes.byref(c), s), lib)
+        _lib.check(lib.qdot_b200_pass2(xp, yp, n, norm, ws, s), lib)
+        if world > 1:
+            torch.distributed.all_reduce(rb)
+        _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, 4196, s), lib)
+    value_check = st.result.value
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = clk.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    p1_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_p1)
+    if world > 1:
+        tt = torch.tensor([ms, p1_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms, p1_ms = float(tt[0]), float(tt[1])
+    value = n_total / (ms * 1e-3)
+    _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, 4196, s), lib)
+    assert st.result.value == value_check, "non-deterministic result"
+
+    # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        xpin = torch.from_numpy(xh).pin_memory()
+        ypin = xpin if args.norm else torch.from_numpy(yh).pin_memory()
+        rep = Q.qdot(xpin, ypin, cfg)  # warm
+        assert rep.value == value_check
+        torch.cuda.synchronize()
+        te = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            rep = Q.qdot(xpin, ypin, cfg)
+        torch.cuda.synchronize()
+        dte = (time.perf_counter() - te) / args.e2e_steps
+        h2d = n * 8 * (1 if args.norm else 2)
+        e2e = {"value": n / dte, "unit": "elements/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 256 + 56 * 64, "ms_per_step": dte * 1e3}
+        del xpin, ypin
+
+    peak, peak_kind = measured_peak()
+    bytes_per_elem = 8 if args.norm else 16
+    achieved = n * bytes_per_elem / (p1_ms * 1e-3) / 1e9
+    traffic, traffic_n = profile_traffic()
+    if traffic is not None and traffic_n and traffic_n != n:
+        traffic = traffic * n / traffic_n
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": "qd::k_pass1",
+                "algorithmic_bytes_per_launch": n * bytes_per_elem, "kernel_ms": p1_ms,
+                "peak_kind": peak_kind, "kernel_share_of_step": p1_ms / ms}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_sample)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": ("C2 qdot n=2^28 fp64 standard-normal per GPU, eps=1e-8, split=none, exact"
+                                    + (" (norm mode x.x)" if args.norm else "")),
+                       "n_per_gpu": n, "n_total": n_total, "epsilon": EPS, "strategy": "exact",
+                       "parallelism": f"dp{world} contiguous shards + NCCL allreduce(hist, partials)",
+                       "l2": "inputs 4 GiB/GPU >> 126 MB L2 (no flush needed)",
+                       "hbm_gbs_step": n * bytes_per_elem * world / (ms * 1e-3) / 1e9 / world},
+            "value_check": value_check,
+            "clocks": clocks,
+            "gpu_launches": 4 * args.steps,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

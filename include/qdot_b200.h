@@ -1,0 +1,171 @@
+/*
+ * qdot_b200.h -- C ABI of the B200-native qdot hot path (sm_100a).
+ *
+ * The reference (qdot 0.1.0, /root/reference/pkg/src/qdot) has no FFI: its
+ * hot path is the Python function
+ *
+ *     qdot(x, y, cfg: ToleranceConfig, strategy=None, reference=None) -> QdotReport
+ *                                                              (kernel.py:179-240)
+ *
+ * whose internal seam is kernel.py:199-202 (select_parameters + the bin_dot
+ * loop + qdot_accumulate).  Every entry point below replaces one stage of
+ * that seam; the Python package paper_2105_00115_b200 (the host-side mirror
+ * of the reference interface) drives them through ctypes, and any other host
+ * language can bind the same symbols.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  `stream` is a cudaStream_t passed as
+ *    void* (NULL = legacy default stream).  x, y are DEVICE pointers to
+ *    float64 unless the function name ends in _host.
+ *  - `ws` is a caller-owned device workspace of qdot_b200_workspace_bytes()
+ *    bytes (256-byte aligned).  All calls are stream-ordered; only
+ *    qdot_b200_fetch / qdot_b200_dot / qdot_b200_dot_host synchronise.
+ *  - Return value: a qdot_status.  Device-detected conditions (non-finite
+ *    input, HALF/SINGLE overflow, eps underflow) are reported in
+ *    qdot_result.status after qdot_b200_fetch; the Python layer maps them to
+ *    the reference's exception types (ValueError / OverflowError).
+ *  - No CPU fallback exists: without a CUDA device every compute entry point
+ *    returns QDOT_ERR_CUDA.
+ */
+#ifndef QDOT_B200_H
+#define QDOT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QDOT_B200_VERSION 1
+
+/* Exponent sums of two finite doubles lie in [-2148, 2046] (floatbits.py:10-14). */
+#define QDOT_KEYS 4195
+#define QDOT_KEY_OFFSET 2148
+
+typedef enum {
+    QDOT_OK = 0,
+    QDOT_ERR_NONFINITE = 1, /* floatbits.py:70-71  ValueError("inputs must be finite")          */
+    QDOT_ERR_OVERFLOW = 2,  /* emulate.py:147-148 / math.ldexp in emulate.py:154 -> OverflowError */
+    QDOT_ERR_ARG = 3,       /* bad config / strategy (scoring.py:72-79, binning.py:131,142)       */
+    QDOT_ERR_CUDA = 4,      /* no device / launch failure                                         */
+    QDOT_ERR_EPS = 5        /* scoring.py:84-85 floor_log2(eps_eff) of 0 -> ValueError            */
+} qdot_status;
+
+/* PrecisionLevel (scoring.py:15-41); values order coarse -> fine */
+typedef enum { QDOT_PERFORATE = 0, QDOT_HALF = 1, QDOT_SINGLE = 2, QDOT_DOUBLE = 3 } qdot_precision;
+
+/* ExactBinning / RangedBinning(width) / BinSplitting(levels)  (binning.py:119-144) */
+typedef enum { QDOT_STRATEGY_EXACT = 0, QDOT_STRATEGY_RANGED = 1, QDOT_STRATEGY_SPLIT = 2 } qdot_strategy;
+
+/* ToleranceConfig (scoring.py:59-79) + the strategy argument of qdot() */
+typedef struct {
+    double epsilon;          /* (0, 2^60]                                      */
+    int32_t split;           /* 0 = SplitMode.NONE, 1 = SplitMode.PER_BIN       */
+    int32_t input_mu;        /* 52, 23 or 10                                    */
+    int32_t strategy;        /* qdot_strategy                                   */
+    int32_t reserved;
+    int64_t strategy_param;  /* width (ranged, >= 1) or levels (split, >= 0)    */
+} qdot_config;
+
+/* One scored bin: Bin (binning.py:168-177) + its bin_dot value (emulate.py:116-154) */
+typedef struct {
+    int64_t lower;       /* bin is the exponent-sum interval (lower, upper]        */
+    int64_t upper;
+    int64_t cardinality; /* M: number of nonzero products in the bin               */
+    int64_t score;       /* bin_score (scoring.py:96-105)                          */
+    int32_t precision;   /* qdot_precision (precision_of, scoring.py:108-123)      */
+    int32_t first_key;   /* first / last present exponent-sum key (e + 2148)       */
+    int32_t last_key;
+    int32_t flags;       /* bit0: HALF bin whose fp32 sequential sum in the
+                            reference is not provably exact (value then agrees
+                            within the bin budget, not necessarily bit-exact)     */
+    double value;        /* per-bin value (already scaled by 2^upper)              */
+} qdot_bin;
+
+/* Everything QdotReport (kernel.py:136-168) needs besides the host-side fsum bounds */
+typedef struct {
+    double value;            /* qdot_accumulate over bins (emulate.py:157-163)   */
+    double eps_eff;          /* scoring.py:193                                    */
+    int64_t n;               /* elements processed                                */
+    int64_t nnz;             /* nonzero products                                  */
+    int64_t zero_count;      /* exact-zero products (ParameterSet.zero_idx.size)  */
+    int64_t counts[4];       /* component counts by precision, zeros -> PERFORATE */
+    int32_t status;          /* qdot_status detected on the device                */
+    int32_t n_bins;
+    int32_t e_min, e_max;    /* 0, 0 when degenerate                              */
+    int32_t early_terminated;
+    int32_t pass2_needed;    /* a second streaming pass was required              */
+    int32_t half_order_sensitive; /* any bin with flags bit0                      */
+    int32_t reserved[5];
+} qdot_result;
+
+/* Workspace regions, in bytes from the start of ws.  Region A (int64[a_len],
+ * exponent histogram + zero count + non-finite count) must be summed across
+ * ranks between pass1 and score; region B (int64[b_len], exact per-key partial
+ * sums) must be summed across ranks between pass2 and finalize.  Both are
+ * integer sums, so any reduction order gives bit-identical results. */
+typedef struct {
+    int64_t total_bytes;
+    int64_t a_offset, a_len;
+    int64_t b_offset, b_len;
+    int64_t result_offset, result_bytes;
+} qdot_ws_layout;
+
+/* --- introspection --------------------------------------------------------- */
+int qdot_b200_version(void);
+const char* qdot_b200_status_string(int status);
+/* message of the last CUDA failure on this host thread */
+const char* qdot_b200_last_error(void);
+size_t qdot_b200_workspace_bytes(void);
+int qdot_b200_workspace_layout(qdot_ws_layout* out);
+/* 0 on success; fills SM count and compute capability of the current device */
+int qdot_b200_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* --- staged path (the seam kernel.py:199-202) -------------------------------- */
+/* zero regions A and B: start of one qdot (per rank) */
+int qdot_b200_begin(void* ws, void* stream);
+/* pass 1 over n elements (accumulates; may be called per chunk/shard):
+ * exponent preprocessing + exact exponent-sum histogram + exact per-key
+ * DOUBLE partials and exact-binning HALF/SINGLE partials.
+ * Replaces floatbits.exponent_preprocess (floatbits.py:57-93),
+ * binning.sorted_bin_init's histogram (binning.py:102-106) and, for every
+ * bin whose products do not depend on the partition, emulate.bin_dot. */
+int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream);
+/* one-CTA scoring on the (reduced) histogram: partition, scores, precisions.
+ * Replaces kernel.select_parameters' partition + scoring (kernel.py:59-72,
+ * binning.py:191-284, scoring.py:126-216).  n_total = elements over all ranks. */
+int qdot_b200_score(void* ws, int64_t n_total, const qdot_config* cfg, void* stream);
+/* pass 2 (exits on the device unless score flagged it): scaled HALF/SINGLE
+ * products for bins whose upper bound differs from the element's exponent
+ * sum (ranged / split / early-terminated bins; emulate.py:137-153). */
+int qdot_b200_pass2(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream);
+/* per-bin values + ascending-upper Neumaier fold (emulate.py:154-163) */
+int qdot_b200_finalize(void* ws, void* stream);
+/* copy the result (and up to max_bins bins) to host memory; synchronises */
+int qdot_b200_fetch(const void* ws, qdot_result* out, qdot_bin* bins, int32_t max_bins, void* stream);
+
+/* --- one-call forms ----------------------------------------------------------- */
+/* device-resident x, y: begin + pass1 + score + pass2 + finalize + fetch */
+int qdot_b200_dot(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
+                  void* ws, qdot_result* out, qdot_bin* bins, int32_t max_bins, void* stream);
+/* host x, y: allocates device buffers, copies in, runs, copies the result out */
+int qdot_b200_dot_host(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
+                       qdot_result* out, qdot_bin* bins, int32_t max_bins);
+
+/* --- lazy Bin.indices support (binning.py:174) ------------------------------- */
+/* write the bin id of every element (-1 for exact-zero products) given a
+ * device LUT of QDOT_KEYS int32 entries mapping exponent-sum key -> bin id
+ * (built by the caller from the bin table: keys first_key..last_key -> bin) */
+int qdot_b200_bin_ids(const double* x, const double* y, int64_t n, int norm, const int32_t* lut_bin,
+                      int32_t* bin_ids, void* stream);
+
+/* --- host-side helpers (no GPU needed; exported for tests and bindings) ----- */
+/* correctly rounded acc * 2^u with math.ldexp semantics; *overflow set on range error */
+double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QDOT_B200_H */

@@ -1,0 +1,291 @@
+// qdot_common.cuh -- constants, workspace layout and exact-arithmetic helpers
+// shared by the sm_100a kernels and the host side of the C ABI.
+//
+// Number formats used throughout:
+//  * key     = exponent sum e = flexp(x) + flexp(y) offset by +2148 into [0, 4195)
+//              (floatbits.py:17-32, 82; sum range floatbits.py:10-14).
+//  * D(e)    = sum over elements with key e of fl(x*y) / 2^qd(e), an exact
+//              integer, qd(e) = max(e - 52, -1074): every fl(x*y) of such an
+//              element is an integer multiple of 2^qd(e) with |k| <= 2^54.
+//  * S0/H0   = exact-binning (u == e) SINGLE / HALF products of the scaled
+//              mantissas (emulate.py:137-146), integers in units of 2^-23 / 2^-10.
+//  * P2(e)   = scaled SINGLE / HALF products for bins with upper u > e, in
+//              units of 2^qs(e,u), qs = max(e - u - mu, 1 - bias - mu).
+// All partials are integers, so every reduction (threads, CTAs, ranks) is
+// exact and order independent.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <cmath>
+
+#include "../../include/qdot_b200.h"
+
+#ifdef __CUDACC__
+#define QD_HD __host__ __device__ __forceinline__
+#else
+#define QD_HD inline
+#endif
+
+namespace qd {
+
+constexpr int KEYS = QDOT_KEYS;
+constexpr int KOFF = QDOT_KEY_OFFSET;
+
+// ---- workspace layout (int64 words unless noted) ---------------------------
+constexpr int64_t A_CNT = 0;            // counts[KEYS]
+constexpr int64_t A_ZERO = KEYS;        // zero-product count
+constexpr int64_t A_NONFINITE = KEYS + 1;
+constexpr int64_t A_LEN = 4224;         // padded
+
+constexpr int64_t B_D0 = 0;             // DOUBLE limbs, weights 2^0, 2^32, 2^64, 2^96
+constexpr int64_t B_D1 = 1 * (int64_t)KEYS;
+constexpr int64_t B_D2 = 2 * (int64_t)KEYS;
+constexpr int64_t B_D3 = 3 * (int64_t)KEYS;
+constexpr int64_t B_S0 = 4 * (int64_t)KEYS;
+constexpr int64_t B_H0 = 5 * (int64_t)KEYS;
+constexpr int64_t B_P2 = 6 * (int64_t)KEYS;
+constexpr int64_t B_INFP = 7 * (int64_t)KEYS;  // +inf DOUBLE products (overflow)
+constexpr int64_t B_INFN = 8 * (int64_t)KEYS;  // -inf DOUBLE products
+constexpr int64_t B_LEN = 37760;        // >= 9*KEYS, padded
+
+// pass-2 descriptor per key (int32): 0 = nothing to do in pass 2
+//   bit 31: needed; bit 16: HALF (else SINGLE); bits 0..15: delta = u - e clamped to 255
+constexpr uint32_t P2_NEED = 0x80000000u;
+constexpr uint32_t P2_HALF = 0x00010000u;
+constexpr int P2_DELTA_MAX = 255;
+
+struct ScoreMeta {         // written by the score kernel, read by pass2 / finalize
+    int32_t status;
+    int32_t n_bins;
+    int32_t e_min, e_max;   // exponent sums (not keys)
+    int32_t early;
+    int32_t need_p2;
+    int32_t degenerate;
+    int32_t input_mu;
+    int64_t nnz;
+    int64_t zero;
+    int64_t n_total;
+    double eps_eff;
+};
+
+constexpr int64_t BYTES_A = A_LEN * 8;
+constexpr int64_t BYTES_B = B_LEN * 8;
+constexpr int64_t OFF_A = 0;
+constexpr int64_t OFF_B = OFF_A + BYTES_A;
+constexpr int64_t OFF_LUT_BIN = OFF_B + BYTES_B;                 // int32[KEYS]
+constexpr int64_t OFF_LUT_P2 = OFF_LUT_BIN + 4224 * 4;           // uint32[KEYS]
+constexpr int64_t OFF_META = OFF_LUT_P2 + 4224 * 4;              // ScoreMeta
+constexpr int64_t OFF_RESULT = OFF_META + 256;                   // qdot_result
+constexpr int64_t OFF_BINS = OFF_RESULT + 256;                   // qdot_bin[KEYS + 1]
+constexpr int64_t BYTES_BINS = (int64_t)sizeof(qdot_bin) * (KEYS + 1);
+constexpr int64_t WS_BYTES = ((OFF_BINS + BYTES_BINS + 255) / 256) * 256;
+
+static_assert(sizeof(ScoreMeta) <= 256, "meta");
+static_assert(sizeof(qdot_result) <= 256, "result");
+static_assert(sizeof(qdot_bin) == 56, "bin layout");
+
+struct WsPtrs {
+    int64_t* a;
+    int64_t* b;
+    int32_t* lut_bin;
+    uint32_t* lut_p2;
+    ScoreMeta* meta;
+    qdot_result* result;
+    qdot_bin* bins;
+};
+
+inline WsPtrs ws_ptrs(void* ws) {
+    char* p = static_cast<char*>(ws);
+    WsPtrs w;
+    w.a = reinterpret_cast<int64_t*>(p + OFF_A);
+    w.b = reinterpret_cast<int64_t*>(p + OFF_B);
+    w.lut_bin = reinterpret_cast<int32_t*>(p + OFF_LUT_BIN);
+    w.lut_p2 = reinterpret_cast<uint32_t*>(p + OFF_LUT_P2);
+    w.meta = reinterpret_cast<ScoreMeta*>(p + OFF_META);
+    w.result = reinterpret_cast<qdot_result*>(p + OFF_RESULT);
+    w.bins = reinterpret_cast<qdot_bin*>(p + OFF_BINS);
+    return w;
+}
+
+// ---- bit helpers -------------------------------------------------------------
+QD_HD uint64_t dbits(double v) {
+#ifdef __CUDA_ARCH__
+    return (uint64_t)__double_as_longlong(v);
+#else
+    uint64_t b; std::memcpy(&b, &v, 8); return b;
+#endif
+}
+QD_HD double bitsd(uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double((long long)b);
+#else
+    double v; std::memcpy(&v, &b, 8); return v;
+#endif
+}
+QD_HD int clz64(uint64_t v) {
+#ifdef __CUDA_ARCH__
+    return __clzll((long long)v);
+#else
+    return v ? __builtin_clzll(v) : 64;
+#endif
+}
+
+// floor(log2|x|) of a nonzero finite double from its bits (floatbits.py:17-27):
+// exponent field - 1023, subnormals via the leading mantissa bit.
+QD_HD int flexp_bits(uint64_t b) {
+    int f = (int)((b >> 52) & 0x7FF);
+    if (f) return f - 1023;
+    uint64_t m = b & ((1ull << 52) - 1);
+    return (63 - clz64(m)) - 1074;
+}
+
+// |x| * 2^-flexp(x) in [1, 2) as raw double bits (exact), x nonzero finite
+QD_HD uint64_t mant_bits(uint64_t b) {
+    int f = (int)((b >> 52) & 0x7FF);
+    uint64_t m = b & ((1ull << 52) - 1);
+    if (!f) {                      // subnormal: normalise the leading 1 to bit 52
+        int sh = clz64(m) - 11;
+        m = (m << sh) & ((1ull << 52) - 1);
+    }
+    return m | (1023ull << 52);
+}
+
+// DOUBLE quantum exponent of key e (see header comment)
+QD_HD int qd_double(int e) { return e - 52 > -1074 ? e - 52 : -1074; }
+
+// fl(x*y) (finite) as an exact integer multiple of 2^qd(e); sign applied
+QD_HD int64_t double_units(uint64_t pb, int e) {
+    int f = (int)((pb >> 52) & 0x7FF);
+    uint64_t m = pb & ((1ull << 52) - 1);
+    if (f) m |= 1ull << 52; else f = 1;
+    int sh = (f - 1075) - qd_double(e);    // 0..2 (product exponent - key)
+    int64_t k = (int64_t)(m << sh);
+    return (pb >> 63) ? -k : k;
+}
+
+// ---- exact rounding -----------------------------------------------------------
+// Round (top + frac) * 2^q, frac in [0,1) nonzero iff `sticky`, to the binary
+// format with `mu` fraction bits and minimum normal exponent `emin`, maximum
+// exponent `emax`: round-to-nearest-even, gradual underflow, overflow -> inf.
+// Returns the rounded value as a double (exact for fp64 and fp32 targets).
+QD_HD double round_scaled(uint64_t top, int q, bool sticky, bool neg, int mu, int emin, int emax,
+                          int* overflow) {
+    if (top == 0) return neg ? -0.0 : 0.0;   // (sticky without top never occurs)
+    int t = 63 - clz64(top);
+    int T = t + q;                              // exponent of the leading bit
+    int qq = (T - mu > emin - mu) ? T - mu : emin - mu;   // quantum exponent
+    int sh = qq - q;
+    uint64_t m;
+    if (sh <= 0) {
+        m = top << (-sh);                        // t <= mu here: exact
+    } else {
+        bool rb, st = sticky;
+        if (sh >= 65) { m = 0; rb = false; st = st || top; }
+        else if (sh == 64) { m = 0; rb = (top >> 63) & 1; st = st || (top & ~(1ull << 63)); }
+        else {
+            m = top >> sh;
+            rb = (top >> (sh - 1)) & 1;
+            st = st || (top & ((1ull << (sh - 1)) - 1));
+        }
+        if (rb && (st || (m & 1))) m += 1;
+    }
+    if (m == 0) return neg ? -0.0 : 0.0;
+    int tm = 63 - clz64(m);
+    if (tm + qq > emax) { if (overflow) *overflow = 1; return neg ? -INFINITY : INFINITY; }
+    double r = ldexp((double)m, qq);             // exact: m <= 2^(mu+1), qq >= -1074
+    return neg ? -r : r;
+}
+
+// math.ldexp(acc, u) semantics: correctly rounded, range error flagged
+QD_HD double ldexp_rn(double acc, int64_t u, int* overflow) {
+    if (acc == 0.0 || !(acc - acc == 0.0)) return acc;   // zero / inf / nan unchanged
+    uint64_t b = dbits(acc);
+    bool neg = b >> 63;
+    int f = (int)((b >> 52) & 0x7FF);
+    uint64_t m = b & ((1ull << 52) - 1);
+    int q;
+    if (f) { m |= 1ull << 52; q = f - 1075; } else { q = -1074; }
+    if (u > 4000) u = 4000;
+    if (u < -4000) u = -4000;
+    return round_scaled(m, q + (int)u, false, neg, 52, -1022, 1023, overflow);
+}
+
+// Exact signed big integer in 32-bit digits held in int64 (carry-save), value
+// = sum d[i] * 2^(32 i + lsb).  Used by finalize for per-bin exact sums.
+template <int ND>
+struct BigSum {
+    int64_t d[ND];
+    int lsb;
+    int nd;
+    QD_HD void init(int lsb_, int ndigits) {
+        lsb = lsb_;
+        nd = ndigits > ND ? ND : ndigits;
+        for (int i = 0; i < nd; ++i) d[i] = 0;
+    }
+    // add v * 2^exp, v a signed 128-bit integer, exp >= lsb
+    QD_HD void add(__int128 v, int exp) {
+        if (v == 0) return;
+        bool neg = v < 0;
+        unsigned __int128 a = neg ? (unsigned __int128)(-v) : (unsigned __int128)v;
+        int pos = exp - lsb;
+        int di = pos >> 5, off = pos & 31;
+        // a << off spans <= 160 bits -> 5 digits
+        unsigned __int128 lo = a << off;
+        uint64_t hi = off ? (uint64_t)(a >> (128 - off)) : 0;
+        uint32_t dg[5] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)(lo >> 64),
+                          (uint32_t)(lo >> 96), (uint32_t)hi};
+        for (int k = 0; k < 5; ++k) {
+            if (di + k >= nd) break;
+            if (neg) d[di + k] -= dg[k]; else d[di + k] += dg[k];
+        }
+    }
+    // normalise, then round to the target format
+    QD_HD double round(int mu, int emin, int emax, int* overflow) {
+        int64_t carry = 0;
+        for (int i = 0; i < nd; ++i) {
+            int64_t v = d[i] + carry;
+            int64_t lo = v & 0xFFFFFFFFll;
+            carry = (v - lo) >> 32;
+            d[i] = lo;
+        }
+        bool neg = carry < 0;   // value = digits + carry * 2^(32 nd)
+        if (neg) {              // two's complement negate digits (carry == -1)
+            int64_t br = 0;
+            for (int i = 0; i < nd; ++i) {
+                int64_t v = -d[i] - br;
+                if (v < 0) { v += 4294967296ll; br = 1; } else br = 0;
+                d[i] = v;
+            }
+        }
+        int top = nd - 1;
+        while (top >= 0 && d[top] == 0) --top;
+        if (top < 0) return 0.0;
+        // gather the top 64 bits below and including the leading digit
+        uint64_t t64 = 0;
+        int got = 0, i = top;
+        bool sticky = false;
+        // leading digit bit length
+        uint32_t lead = (uint32_t)d[top];
+        int lb = 32 - (lead ? clz64((uint64_t)lead) - 32 : 32);
+        t64 = lead;
+        got = lb;
+        --i;
+        while (i >= 0 && got + 32 <= 64) { t64 = (t64 << 32) | (uint32_t)d[i]; got += 32; --i; }
+        int q;
+        if (i >= 0 && got < 64) {          // take the high (64-got) bits of the next digit
+            int take = 64 - got;
+            uint32_t nx = (uint32_t)d[i];
+            t64 = (t64 << take) | (nx >> (32 - take));
+            sticky = (nx & ((1u << (32 - take)) - 1)) != 0;
+            q = lsb + 32 * i + (32 - take);
+            --i;
+        } else {
+            q = lsb + 32 * (i + 1);
+        }
+        while (i >= 0 && !sticky) { sticky = d[i] != 0; --i; }
+        return round_scaled(t64, q, sticky, neg, mu, emin, emax, overflow);
+    }
+};
+
+}  // namespace qd

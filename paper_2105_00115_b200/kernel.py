@@ -1,0 +1,237 @@
+"""qdot entry point: the drop-in replacement for the reference's kernel.qdot.
+
+    qdot(x, y, cfg, strategy=None, reference=None) -> QdotReport   (kernel.py:179-240)
+    select_parameters(x, y, cfg, strategy=None) -> ParameterSet    (kernel.py:34-72)
+
+Same signature, argument meaning, report fields and exception types as the
+reference.  Underneath, one call is (csrc/, include/qdot_b200.h):
+
+    begin -> pass1 (stream x, y once: histogram + exact per-key partials)
+          -> score (one CTA: partition, scores, precisions)
+          -> pass2 (only if a HALF/SINGLE bin has upper != e for a member)
+          -> finalize (per-bin values, Neumaier fold) -> fetch (small D2H)
+
+The report's bounds are computed here with math.fsum over the per-bin terms
+exactly as kernel.py:205-222 does.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Dict, Optional
+
+import numpy as np
+
+from . import _lib
+from .binning import Bin, ExactBinning, Strategy, strategy_label
+from .device import as_device_vector, config_struct, require_cuda, stream_handle, thread_state
+from .scoring import (ParameterSet, PrecisionLevel, SplitMode, ToleranceConfig, absolute_bound_term,
+                      relative_bound_term)
+
+__all__ = ["QdotReport", "qdot", "select_parameters", "run_device"]
+
+
+@dataclass
+class QdotReport:
+    """Value plus everything needed to audit it (kernel.py:136-168)."""
+
+    value: float
+    counts: Dict[PrecisionLevel, int]
+    abs_bound: float
+    rel_bound: float
+    abs_cap: float
+    rel_guarantee: float
+    rel_hypothesis: str
+    rel_bound_e: Optional[float]
+    early_terminated: bool
+    n: int
+    epsilon: float
+    split: SplitMode
+    strategy: str
+    phase_ns: Dict[str, int] = field(default_factory=dict)
+    params: Optional[ParameterSet] = None
+    # B200 extras (not in the reference report)
+    pass2_needed: bool = False
+    half_order_sensitive: bool = False
+
+    def count(self, level: PrecisionLevel) -> int:
+        return self.counts.get(level, 0)
+
+    def fraction(self, level: PrecisionLevel) -> float:
+        return self.count(level) / self.n if self.n else 0.0
+
+
+class _Indexer:
+    """Materialises Bin.indices / ParameterSet.zero_idx on first access with a
+    device pass (qdot_b200_bin_ids) and a stable device sort by bin id."""
+
+    def __init__(self, xd, yd, n, norm, device):
+        self.xd, self.yd, self.n, self.norm, self.device = xd, yd, n, norm, device
+        self.done = False
+
+    def materialize(self, params: ParameterSet) -> None:
+        if self.done:
+            return
+        import torch
+        lib = _lib.load()
+        lut = np.full(_lib.KEYS, -1, dtype=np.int32)
+        for b_id, b in enumerate(params.bins):
+            lut[b.first_key:b.last_key + 1] = b_id
+        lut_d = torch.from_numpy(lut).to(self.device)
+        ids = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.device)
+        st = stream_handle(self.device)
+        _lib.check(lib.qdot_b200_bin_ids(self.xd.data_ptr(), self.yd.data_ptr(), self.n, int(self.norm),
+                                         lut_d.data_ptr(), ids.data_ptr(), st), lib)
+        order = torch.sort(ids[:self.n], stable=True).indices.cpu().numpy().astype(np.int64)
+        pos = params.zero_count
+        params._zero_idx = order[:pos].copy()
+        for b in params.bins:
+            b.indices = order[pos:pos + b.cardinality].copy()
+            pos += b.cardinality
+        self.done = True
+        self.xd = self.yd = None
+
+
+def run_device(xd, yd, n: int, norm: bool, cfg: ToleranceConfig, strategy, st=None, timing: bool = True,
+               stream=None):
+    """Launch the whole device pipeline on device vectors; returns (result, bins, phase_ns)."""
+    lib = _lib.load()
+    if st is None:
+        st = thread_state(xd.device)
+    c = config_struct(cfg, strategy)
+    s = stream_handle(xd.device) if stream is None else int(stream)
+    ws = st.ws_ptr
+    xp = xd.data_ptr()
+    yp = xp if norm else yd.data_ptr()
+    torch_stream = None
+    if timing:
+        import torch
+        torch_stream = torch.cuda.current_stream(xd.device) if stream is None else None
+        if torch_stream is not None:
+            st.ev[0].record(torch_stream)
+    _lib.check(lib.qdot_b200_begin(ws, s), lib)
+    _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(norm), ws, s), lib)
+    _lib.check(lib.qdot_b200_score(ws, n, ctypes.byref(c), s), lib)
+    if torch_stream is not None:
+        st.ev[1].record(torch_stream)
+    _lib.check(lib.qdot_b200_pass2(xp, yp, n, int(norm), ws, s), lib)
+    _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+    if torch_stream is not None:
+        st.ev[2].record(torch_stream)
+    _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
+    phase = {"select": 0, "compute": 0, "reference": 0}
+    if torch_stream is not None:
+        phase["select"] = int(st.ev[0].elapsed_time(st.ev[1]) * 1e6)
+        phase["compute"] = int(st.ev[1].elapsed_time(st.ev[2]) * 1e6)
+    return st.result, st.bins, phase
+
+
+def _build_params(res, cbins, cfg, strategy, indexer) -> ParameterSet:
+    ps = ParameterSet(bins=[], e_min=int(res.e_min), e_max=int(res.e_max), strategy=strategy, tolerance=cfg,
+                      early_terminated=bool(res.early_terminated), n=int(res.n), eps_eff=float(res.eps_eff),
+                      n_bins=int(res.n_bins), zero_count=int(res.zero_count), _indexer=indexer)
+    bins = []
+    for i in range(res.n_bins):
+        cb = cbins[i]
+        bins.append(Bin(lower=int(cb.lower), upper=int(cb.upper), cardinality=int(cb.cardinality),
+                        score=int(cb.score), precision=PrecisionLevel.from_code(cb.precision),
+                        value=float(cb.value), flags=int(cb.flags), first_key=int(cb.first_key),
+                        last_key=int(cb.last_key), indexer=indexer, owner=ps))
+    ps.bins = bins
+    # ParameterSet.rel_bound: plain left-to-right sum (scoring.py:195-199)
+    rb = 0.0
+    for b in bins:
+        rb += relative_bound_term(b, ps.e_max)
+    ps.rel_bound = rb
+    return ps
+
+
+def _prepare(x, y):
+    torch = require_cuda()
+    is_norm = x is y                                           # kernel.py:194
+    device = torch.device("cuda", torch.cuda.current_device())
+    xd, _ = as_device_vector(x, device)
+    yd = xd if is_norm else as_device_vector(y, device)[0]
+    if xd.shape[0] != yd.shape[0]:                             # floatbits.py:68-69
+        raise ValueError(f"length mismatch: {xd.shape[0]} vs {yd.shape[0]}")
+    return is_norm, xd, yd
+
+
+def select_parameters(x, y, cfg: ToleranceConfig, strategy: Strategy = None) -> ParameterSet:
+    """Parameter selection only (kernel.py:34-72): pass1 + score on the device."""
+    if strategy is None:
+        strategy = ExactBinning()
+    is_norm, xd, yd = _prepare(x, y)
+    n = int(xd.shape[0])
+    lib = _lib.load()
+    st = thread_state(xd.device)
+    c = config_struct(cfg, strategy)
+    s = stream_handle(xd.device)
+    ws = st.ws_ptr
+    _lib.check(lib.qdot_b200_begin(ws, s), lib)
+    _lib.check(lib.qdot_b200_pass1(xd.data_ptr(), yd.data_ptr(), n, int(is_norm), ws, s), lib)
+    _lib.check(lib.qdot_b200_score(ws, n, ctypes.byref(c), s), lib)
+    # finalize also fills the result header and per-bin values; cheap (1 CTA)
+    _lib.check(lib.qdot_b200_pass2(xd.data_ptr(), yd.data_ptr(), n, int(is_norm), ws, s), lib)
+    _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+    _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
+    res = st.result
+    _raise_status(res)
+    indexer = _Indexer(xd, yd, n, is_norm, xd.device)
+    return _build_params(res, st.bins, cfg, strategy, indexer)
+
+
+def _raise_status(res) -> None:
+    if res.status == _lib.QDOT_ERR_OVERFLOW:
+        raise OverflowError("math range error")
+    _lib.check(int(res.status))
+
+
+def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer) -> QdotReport:
+    """Host-side report assembly (kernel.py:205-240)."""
+    params = _build_params(res, cbins, cfg, strategy, indexer)
+    abs_bound = math.fsum(absolute_bound_term(b) for b in params.bins)
+    rel_bound = math.fsum(relative_bound_term(b, params.e_max) for b in params.bins)
+    rel_hypothesis = "assumed"
+    rel_bound_e = None
+    if is_norm:
+        rel_hypothesis = "holds"
+    if reference is not None:
+        fe = getattr(reference, "flexp_e", None)
+        if fe is None:
+            rel_hypothesis = "violated" if not is_norm else rel_hypothesis
+        else:
+            holds = params.e_max <= fe or not params.bins
+            rel_hypothesis = "holds" if (holds or is_norm) else "violated"
+            rel_bound_e = math.fsum(b.cardinality * math.ldexp(b.precision.eps, b.upper - fe + 1)
+                                    for b in params.bins)
+    counts = {level: 0 for level in PrecisionLevel}
+    for i, level in enumerate((PrecisionLevel.PERFORATE, PrecisionLevel.HALF, PrecisionLevel.SINGLE,
+                               PrecisionLevel.DOUBLE)):
+        counts[level] = int(res.counts[i])
+    return QdotReport(
+        value=float(res.value), counts=counts, abs_bound=abs_bound, rel_bound=rel_bound,
+        abs_cap=2.0 * abs_bound, rel_guarantee=params.rel_guarantee, rel_hypothesis=rel_hypothesis,
+        rel_bound_e=rel_bound_e, early_terminated=params.early_terminated, n=params.n,
+        epsilon=cfg.epsilon, split=cfg.split, strategy=strategy_label(params.strategy),
+        phase_ns=phase, params=params, pass2_needed=bool(res.pass2_needed),
+        half_order_sensitive=bool(res.half_order_sensitive))
+
+
+def qdot(x, y, cfg: ToleranceConfig, strategy: Strategy = None, reference=None) -> QdotReport:
+    """Approximate dot product with audit report (kernel.py:179-240).
+
+    x, y: array-likes (coerced like np.ascontiguousarray(float64) and copied
+    to the current CUDA device) or CUDA/CPU torch tensors (float64 CUDA
+    tensors are used in place).  ``x is y`` selects norm mode (one read).
+    """
+    if strategy is None:
+        strategy = ExactBinning()
+    is_norm, xd, yd = _prepare(x, y)
+    n = int(xd.shape[0])
+    res, cbins, phase = run_device(xd, yd, n, is_norm, cfg, strategy)
+    _raise_status(res)
+    indexer = _Indexer(xd, yd, n, is_norm, xd.device)
+    return report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer)

@@ -1,0 +1,248 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+golden outputs and the CPU oracle.
+
+Bar: bins, scores, precisions, counts, bounds and
+error behaviour bit-exact; per-bin values and the final value bit-exact
+wherever the reference's own accumulation is exact (always for SINGLE /
+DOUBLE in practice; HALF bins flagged order-sensitive fall back to the
+per-bin budget M * 2^(u+1) * eps); every value within abs_cap of the
+reference value and of the exact dot.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import golden_util as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2105_00115_b200 as Q  # noqa: E402
+from paper_2105_00115_b200 import PrecisionLevel as P  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+PREC = {0: P.PERFORATE, 1: P.HALF, 2: P.SINGLE, 3: P.DOUBLE}
+LABEL = {P.PERFORATE: "perforate", P.HALF: "half", P.SINGLE: "single", P.DOUBLE: "double"}
+
+
+def strat(s):
+    return Q.parse_strategy(s)
+
+
+def cfg_of(case):
+    return Q.ToleranceConfig(epsilon=G.hexf(case["epsilon"]),
+                             split=Q.SplitMode.PER_BIN if case["split"] == "per-bin" else Q.SplitMode.NONE,
+                             input_mu=case["input_mu"])
+
+
+def same(a, b):
+    return a == b or (math.isnan(a) and math.isnan(b))
+
+
+def check_against_golden(case, rep):
+    bins = rep.params.bins
+    got = [[b.lower, b.upper, b.cardinality, b.score, b.precision.code] for b in bins]
+    assert got == [w[:5] for w in case["bins"]], case["name"]
+    assert rep.params.n_bins == case["n_bins"]
+    assert rep.early_terminated == case["early_terminated"]
+    assert rep.params.eps_eff == G.hexf(case["eps_eff"])
+    if case["n_bins"]:
+        assert (rep.params.e_min, rep.params.e_max) == (case["e_min"], case["e_max"])
+    assert rep.params.zero_count == case["zero_count"]
+    assert {LABEL[k]: v for k, v in rep.counts.items()} == case["counts"]
+    assert rep.abs_bound == G.hexf(case["abs_bound"])
+    assert rep.rel_bound == G.hexf(case["rel_bound"])
+    assert rep.rel_guarantee == G.hexf(case["rel_guarantee"])
+    assert rep.abs_cap == G.hexf(case["abs_cap"])
+    # per-bin values
+    exact_bins = True
+    for b, w in zip(bins, case["bins"]):
+        want = G.hexf(w[5])
+        if same(b.value, want):
+            continue
+        exact_bins = False
+        assert b.flags & 1 or b.precision is P.DOUBLE, (case["name"], b, b.value, want)
+        budget = b.cardinality * math.ldexp(b.precision.eps, b.upper + 1)
+        assert abs(b.value - want) <= budget, (case["name"], b)
+    want = G.hexf(case["value"])
+    if exact_bins:
+        assert same(rep.value, want), (case["name"], rep.value.hex(), case["value"])
+    else:
+        assert abs(rep.value - want) <= rep.abs_cap
+    if case.get("exact") is not None and math.isfinite(rep.value):
+        assert abs(rep.value - G.hexf(case["exact"])) <= rep.abs_cap + 1e-300
+
+
+CASES = G.select(max_n=1 << 20)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_golden_case(case):
+    x, y = G.inputs(case)
+    cfg = cfg_of(case)
+    yy = x if case["norm"] else y
+    if "error" in case:
+        exc = {"ValueError": ValueError, "OverflowError": OverflowError}[case["error"]]
+        with pytest.raises(exc):
+            Q.qdot(x, yy, cfg, strategy=strat(case["strategy"]))
+        return
+    rep = Q.qdot(x, yy, cfg, strategy=strat(case["strategy"]))
+    check_against_golden(case, rep)
+    assert rep.rel_hypothesis == case["rel_hypothesis"]
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("strategy", ["exact", "ranged:3", "split:4"])
+def test_random_against_oracle(seed, strategy):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(1, 20000))
+    t = int(rng.integers(0, 120))
+    x = np.ldexp(rng.uniform(0.5, 1, n) * rng.choice([-1, 1], n), rng.integers(-t // 2, t // 2 + 1, n))
+    y = np.ldexp(rng.uniform(0.5, 1, n), rng.integers(-t // 2, t // 2 + 1, n))
+    if seed % 3 == 0:
+        x[rng.integers(0, n, max(1, n // 50))] = 0.0
+    eps = float(np.ldexp(1.0, -int(rng.integers(0, 55))))
+    split = "per-bin" if seed % 2 else "none"
+    r = O.qdot(x, y, eps, split, 52, strategy)
+    rep = Q.qdot(x, y, Q.ToleranceConfig(eps, Q.SplitMode(split)), strategy=strat(strategy))
+    assert [[b.lower, b.upper, b.cardinality, b.score, b.precision.code] for b in rep.params.bins] == \
+        [[b.lower, b.upper, b.cardinality, b.score, b.precision] for b in r.bins]
+    for b, w in zip(rep.params.bins, r.bins):
+        if not same(b.value, w.value):
+            assert b.flags & 1 or b.precision is P.DOUBLE
+            assert abs(b.value - w.value) <= b.cardinality * math.ldexp(b.precision.eps, b.upper + 1)
+    assert abs(rep.value - r.value) <= rep.abs_cap
+    ex, _, _ = O.exact_dot(x, y)
+    assert abs(rep.value - ex) <= rep.abs_cap
+
+
+def test_toy_bit_exact():
+    x = np.array([2.0**27, 2.0**8, 2.0**-3, 2.0**20])
+    y = np.array([2.0**23, 2.0**-14, 2.0**7, 2.0**-3])
+    rep = Q.qdot(x, y, Q.ToleranceConfig(2.0**-34))
+    assert rep.value == 2.0**50 + 2.0**17
+    assert [b.score for b in rep.params.bins] == [-21, -11, 2, 35]
+    assert rep.rel_bound == 2.0**-51 + 2.0**-42 + 2.0**-45 + 2.0**-55
+    assert set(rep.phase_ns) == {"select", "compute", "reference"}
+
+
+def test_norm_mode_reads_once_and_matches():
+    x, _ = O.gen_normal(1 << 16, seed=5)
+    a = Q.qdot(x, x, Q.ToleranceConfig(1e-8))
+    b = Q.qdot(x, x.copy(), Q.ToleranceConfig(1e-8))
+    assert a.value == b.value and a.rel_hypothesis == "holds" and b.rel_hypothesis == "assumed"
+    r = O.qdot(x, x, 1e-8)
+    assert a.value == r.value
+
+
+def test_torch_inputs_and_misaligned_views():
+    x, y = O.gen_normal((1 << 15) + 7, seed=9)
+    want = O.qdot(x[1:], y[1:], 1e-9).value
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.from_numpy(y).cuda()
+    rep = Q.qdot(xt[1:], yt[1:], Q.ToleranceConfig(1e-9))     # 8-byte aligned: scalar loads
+    assert rep.value == want
+    rep2 = Q.qdot(xt[1:].clone(), yt[1:].clone(), Q.ToleranceConfig(1e-9))
+    assert rep2.value == want
+
+
+def test_lazy_indices_match_oracle():
+    for strategy in ["exact", "ranged:4", "split:3"]:
+        x, y = O.gen_family("B", 12, 5000, 77)
+        x[::97] = 0.0
+        r = O.qdot(x, y, 1e-6, "none", 52, strategy, members=True)
+        rep = Q.qdot(x, y, Q.ToleranceConfig(1e-6), strategy=strat(strategy))
+        for b, w in zip(rep.params.bins, r.bins):
+            assert b.indices.tolist() == w.indices.tolist()
+        assert rep.params.zero_idx.tolist() == np.flatnonzero((x == 0) | (y == 0)).tolist()
+
+
+def test_errors():
+    with pytest.raises(ValueError):
+        Q.qdot(np.array([1.0, np.nan]), np.ones(2), Q.ToleranceConfig(1e-3))
+    with pytest.raises(ValueError):
+        Q.qdot(np.ones(3), np.ones(4), Q.ToleranceConfig(1e-3))
+    with pytest.raises(ValueError):
+        Q.qdot(np.ones((2, 2)), np.ones((2, 2)), Q.ToleranceConfig(1e-3))
+    with pytest.raises(TypeError):
+        Q.qdot(np.ones(3), np.ones(3), Q.ToleranceConfig(1e-3), strategy=object())
+
+
+def test_empty_and_all_zero():
+    rep = Q.qdot(np.zeros(0), np.zeros(0), Q.ToleranceConfig(2.0**-34))
+    assert rep.value == 0.0 and rep.n == 0 and sum(rep.counts.values()) == 0
+    rep = Q.qdot(np.zeros(4), np.ones(4), Q.ToleranceConfig(2.0**-34))
+    assert rep.value == 0.0 and rep.counts[P.PERFORATE] == 4 and rep.abs_bound == 0.0
+
+
+def test_sharded_tables_sum_like_one_device():
+    """The multi-GPU exchange is an integer sum of regions A and B: emulate two
+    ranks on one device and check bit-identical results to the single call."""
+    import ctypes
+    from paper_2105_00115_b200 import _lib
+    from paper_2105_00115_b200.device import ThreadState, config_struct
+    lib = _lib.load()
+    x, y = O.gen_illcond(1 << 18, seed=3)
+    cfg = Q.ToleranceConfig(1e-12)
+    whole = Q.qdot(x, y, cfg)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    xd = torch.from_numpy(x).to(dev)
+    yd = torch.from_numpy(y).to(dev)
+    n = x.shape[0]
+    cut = n // 3
+    ranks = [ThreadState(dev), ThreadState(dev)]
+    s = torch.cuda.current_stream().cuda_stream
+    parts = [(0, cut), (cut, n)]
+    for st, (a, b) in zip(ranks, parts):
+        _lib.check(lib.qdot_b200_begin(st.ws_ptr, s))
+        _lib.check(lib.qdot_b200_pass1(xd[a:].data_ptr(), yd[a:].data_ptr(), b - a, 0, st.ws_ptr, s))
+    ra = ranks[0].region_a() + ranks[1].region_a()          # "allreduce" of region A
+    for st in ranks:
+        st.region_a().copy_(ra)
+    c = config_struct(cfg, Q.ExactBinning())
+    for st, (a, b) in zip(ranks, parts):
+        _lib.check(lib.qdot_b200_score(st.ws_ptr, n, ctypes.byref(c), s))
+        _lib.check(lib.qdot_b200_pass2(xd[a:].data_ptr(), yd[a:].data_ptr(), b - a, 0, st.ws_ptr, s))
+    rb = ranks[0].region_b() + ranks[1].region_b()          # "allreduce" of region B
+    for st in ranks:
+        st.region_b().copy_(rb)
+        _lib.check(lib.qdot_b200_finalize(st.ws_ptr, s))
+        _lib.check(lib.qdot_b200_fetch(st.ws_ptr, ctypes.byref(st.result), st.bins, 4196, s))
+        assert st.result.value == whole.value
+        assert st.result.n_bins == whole.params.n_bins
+
+
+def test_c1_against_golden_and_exact():
+    case = next(c for c in G.cases() if c["name"] == "C1_none")
+    x, y = G.inputs(case)
+    rep = Q.qdot(x, y, cfg_of(case))
+    assert rep.value == G.hexf(case["value"])                  # -979.5638873355846
+    assert rep.value == -979.5638873355846
+
+
+@pytest.mark.slow
+def test_c2_headline_size_properties():
+    """n = 2^28 (BASELINE configs[1]): bins and precisions equal the oracle's,
+    value equals the oracle's reference-order value and lies within abs_cap of
+    the exact dot; repeated runs are bit-identical."""
+    n = 1 << 28
+    x, y = O.gen_normal(n, seed=0)
+    O.set_threads(32)
+    r = O.qdot(x, y, 1e-8)
+    ex, _, _ = O.exact_dot(x, y)
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.from_numpy(y).cuda()
+    del x, y
+    cfg = Q.ToleranceConfig(1e-8)
+    rep = Q.qdot(xt, yt, cfg)
+    rep2 = Q.qdot(xt, yt, cfg)
+    assert rep.value == rep2.value
+    assert [[b.lower, b.upper, b.cardinality, b.score, b.precision.code] for b in rep.params.bins] == \
+        [[b.lower, b.upper, b.cardinality, b.score, b.precision] for b in r.bins]
+    assert rep.value == r.value == -23532.7407708119
+    assert abs(rep.value - ex) <= rep.abs_cap
