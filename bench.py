@@ -227,7 +227,7 @@ def main():
         _lib.check(lib.qdot_b200_begin(ws, s), lib)
         if i is not None:
             ev_p1[i][0].record(stream)
-        _lib.check(lib.qdot_b200_pass1(xp, yp, n, norm, ws, s), lib)
+        _lib.check(lib.qdot_b200_pass1(xp, yp, n, norm, ctypes.byref(c), n_total, ws, s), lib)
         if i is not None:
             ev_p1[i][1].record(stream)
         if world > 1:
@@ -270,6 +270,9 @@ def main():
     value = n_total / (ms * 1e-3)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, 4196, s), lib)
     assert st.result.value == value_check, "non-deterministic result"
+    a_host = ra.cpu()
+    pass1_modes = {"full_ctas": int(a_host[_lib.KEYS + 2]), "lean_ctas": int(a_host[_lib.KEYS + 3]),
+                   "pass2_needed": bool(st.result.pass2_needed)}
 
     # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region
     e2e = None
@@ -314,6 +317,7 @@ def main():
                        "l2": "inputs 4 GiB/GPU >> 126 MB L2 (no flush needed)",
                        "hbm_gbs_step": n * bytes_per_elem * world / (ms * 1e-3) / 1e9 / world},
             "value_check": value_check,
+            "pass1_modes": pass1_modes,
             "clocks": clocks,
             "gpu_launches": 4 * args.steps,
             "roofline": roofline,

@@ -64,7 +64,7 @@ typedef struct {
     int32_t split;           /* 0 = SplitMode.NONE, 1 = SplitMode.PER_BIN       */
     int32_t input_mu;        /* 52, 23 or 10                                    */
     int32_t strategy;        /* qdot_strategy                                   */
-    int32_t reserved;
+    int32_t reserved;        /* pass-1 mode hint: 0 auto, 1 lean, 2 full        */
     int64_t strategy_param;  /* width (ranged, >= 1) or levels (split, >= 0)    */
 } qdot_config;
 
@@ -130,8 +130,12 @@ int qdot_b200_begin(void* ws, void* stream);
  * DOUBLE partials and exact-binning HALF/SINGLE partials.
  * Replaces floatbits.exponent_preprocess (floatbits.py:57-93),
  * binning.sorted_bin_init's histogram (binning.py:102-106) and, for every
- * bin whose products do not depend on the partition, emulate.bin_dot. */
-int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream);
+ * bin whose products do not depend on the partition, emulate.bin_dot.
+ * cfg (may be NULL) and n_total (elements over all ranks) only steer the
+ * per-CTA lean/full choice (speed, never results); cfg->reserved = 0 auto,
+ * 1 lean, 2 full. */
+int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
+                    int64_t n_total, void* ws, void* stream);
 /* one-CTA scoring on the (reduced) histogram: partition, scores, precisions.
  * Replaces kernel.select_parameters' partition + scoring (kernel.py:59-72,
  * binning.py:191-284, scoring.py:126-216).  n_total = elements over all ranks. */

@@ -64,7 +64,7 @@ SIGNATURES = {
     "qdot_b200_workspace_layout": (_I, [ctypes.POINTER(QdotWsLayout)]),
     "qdot_b200_device_info": (_I, [ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "qdot_b200_begin": (_I, [_P, _P]),
-    "qdot_b200_pass1": (_I, [_P, _P, _I64, _I, _P, _P]),
+    "qdot_b200_pass1": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _I64, _P, _P]),
     "qdot_b200_score": (_I, [_P, _I64, ctypes.POINTER(QdotConfig), _P]),
     "qdot_b200_pass2": (_I, [_P, _P, _I64, _I, _P, _P]),
     "qdot_b200_finalize": (_I, [_P, _P]),

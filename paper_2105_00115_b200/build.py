@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libqdot_b200.so")
 SOURCES = ["qdot_kernels.cu", "qdot_capi.cu"]
-HEADERS = ["qdot_common.cuh", "qdot_kernels.h"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) if os.path.isdir(CSRC) else []
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -111,10 +111,24 @@ int qdot_b200_begin(void* ws, void* stream) {
     return QDOT_OK;
 }
 
-int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream) {
+int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
+                    int64_t n_total, void* ws, void* stream) {
     if (!ws || n < 0 || (n > 0 && (!x || (!norm && !y)))) return QDOT_ERR_ARG;
+    P1Params prm;
+    prm.epsilon = 1.0;
+    prm.input_mu = 52;
+    prm.mode = 1;   // no config: lean
+    prm.n_total = n_total > n ? n_total : n;
+    if (cfg) {
+        int v = validate(cfg);
+        if (v) return v;
+        prm.epsilon = cfg->epsilon;
+        prm.input_mu = cfg->input_mu;
+        prm.mode = cfg->reserved;   // 0 auto, 1 lean, 2 full (testing knob)
+        if (prm.mode < 0 || prm.mode > 2) return QDOT_ERR_ARG;
+    }
     WsPtrs w = ws_ptrs(ws);
-    QD_CHECK(launch_pass1(x, norm ? x : y, n, norm != 0, w.a, w.b, static_cast<cudaStream_t>(stream)), "pass1");
+    QD_CHECK(launch_pass1(x, norm ? x : y, n, norm != 0, w.a, w.b, prm, static_cast<cudaStream_t>(stream)), "pass1");
     return QDOT_OK;
 }
 
@@ -139,7 +153,8 @@ int qdot_b200_pass2(const double* x, const double* y, int64_t n, int norm, void*
 int qdot_b200_finalize(void* ws, void* stream) {
     if (!ws) return QDOT_ERR_ARG;
     WsPtrs w = ws_ptrs(ws);
-    QD_CHECK(launch_finalize(w.a, w.b, w.meta, w.result, w.bins, static_cast<cudaStream_t>(stream)), "finalize");
+    QD_CHECK(launch_finalize(w.a, w.b, w.lut_p2, w.meta, w.result, w.bins, static_cast<cudaStream_t>(stream)),
+             "finalize");
     return QDOT_OK;
 }
 
@@ -170,7 +185,7 @@ int qdot_b200_dot(const double* x, const double* y, int64_t n, int norm, const q
     if (v) return v;
     int r;
     if ((r = qdot_b200_begin(ws, stream))) return r;
-    if ((r = qdot_b200_pass1(x, y, n, norm, ws, stream))) return r;
+    if ((r = qdot_b200_pass1(x, y, n, norm, cfg, n, ws, stream))) return r;
     if ((r = qdot_b200_score(ws, n, cfg, stream))) return r;
     if ((r = qdot_b200_pass2(x, y, n, norm, ws, stream))) return r;
     if ((r = qdot_b200_finalize(ws, stream))) return r;
@@ -214,7 +229,7 @@ int qdot_b200_dot_host(const double* hx, const double* hy, int64_t n, int norm, 
         }
         cudaEventRecord(ev, cs);
         cudaStreamWaitEvent(ks, ev, 0);
-        if ((rc = qdot_b200_pass1(dx + off, norm ? nullptr : dy + off, len, norm, ws, ks))) goto out_;
+        if ((rc = qdot_b200_pass1(dx + off, norm ? nullptr : dy + off, len, norm, cfg, n, ws, ks))) goto out_;
     }
     if ((rc = qdot_b200_score(ws, n, cfg, ks))) goto out_;
     if ((rc = qdot_b200_pass2(dx, norm ? nullptr : dy, n, norm, ws, ks))) goto out_;

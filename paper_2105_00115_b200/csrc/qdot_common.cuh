@@ -36,7 +36,11 @@ constexpr int KOFF = QDOT_KEY_OFFSET;
 constexpr int64_t A_CNT = 0;            // counts[KEYS]
 constexpr int64_t A_ZERO = KEYS;        // zero-product count
 constexpr int64_t A_NONFINITE = KEYS + 1;
-constexpr int64_t A_LEN = 4224;         // padded
+constexpr int64_t A_FULLCTAS = KEYS + 2;  // pass-1 CTAs that ran the full-variant loop (diagnostic)
+constexpr int64_t A_LEANCTAS = KEYS + 3;  // pass-1 CTAs that ran the lean loop (diagnostic)
+constexpr int64_t A_HOT = 4224;         // [KEYS]: elements of the key accumulated by a lean
+                                        // private window (exact HALF/SINGLE variants absent)
+constexpr int64_t A_LEN = 8448;         // padded
 
 constexpr int64_t B_D0 = 0;             // DOUBLE limbs, weights 2^0, 2^32, 2^64, 2^96
 constexpr int64_t B_D1 = 1 * (int64_t)KEYS;
@@ -54,6 +58,14 @@ constexpr int64_t B_LEN = 37760;        // >= 9*KEYS, padded
 constexpr uint32_t P2_NEED = 0x80000000u;
 constexpr uint32_t P2_HALF = 0x00010000u;
 constexpr int P2_DELTA_MAX = 255;
+
+// pass-1 parameters (what the per-CTA lean/full decision needs)
+struct P1Params {
+    double epsilon;
+    int64_t n_total;
+    int32_t input_mu;
+    int32_t mode;            // 0 auto, 1 force lean, 2 force full variants
+};
 
 struct ScoreMeta {         // written by the score kernel, read by pass2 / finalize
     int32_t status;

@@ -16,6 +16,8 @@
 //   bin_ids   lazy Bin.indices support (binning.py:174).
 //
 // No tensor cores: this is a memory-bound integer/bit reduction.
+#include <cstdlib>
+
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -24,351 +26,7 @@
 
 namespace qd {
 
-// =============================================================================
-// pass 1
-// =============================================================================
-constexpr int P1_T = 256;                    // threads per CTA
-constexpr int P1_W = 16;                     // keys with per-thread private slots
-constexpr int P1_CW = 192;                   // keys with per-CTA smem-atomic slots
-constexpr int P1_V = 4;                      // 16-byte vectors per thread per tile per operand
-constexpr int P1_EPT = 2 * P1_V;             // elements per thread per tile
-constexpr int P1_TILE = P1_T * P1_EPT;       // elements per tile
-constexpr int P1_FLUSH = 255 / P1_EPT;       // tiles between flushes (<= 255 elements/thread)
-
-struct __align__(16) P1Shared {
-    ulonglong2 priv[P1_W * P1_T];            // .x = DOUBLE units (int64), .y = packed S|H|count
-    __int128 t_d[P1_W];                      // CTA totals of the private window
-    long long t_s[P1_W], t_h[P1_W], t_c[P1_W];
-    unsigned long long c_cnt[P1_CW];         // cold window (smem atomics)
-    unsigned long long c_dlo[P1_CW];
-    unsigned long long c_dhi[P1_CW];
-    unsigned long long c_s[P1_CW];
-    unsigned long long c_h[P1_CW];
-    unsigned long long red[2 * (P1_T / 32)];
-    int base;                                // first key of the private window
-    int cbase;                               // first key of the cold window
-    int pick[2];
-};
-
-size_t pass1_smem_bytes() { return sizeof(P1Shared); }
-
-// push one key's exact partials to the global tables (region A / B)
-__device__ __forceinline__ void push_key(int64_t* __restrict__ A, int64_t* __restrict__ B, int key,
-                                         unsigned long long cnt, __int128 d, long long s, long long h) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(A + A_CNT + key), cnt);
-    unsigned long long l0 = (unsigned long long)(uint32_t)(uint64_t)d;
-    unsigned long long l1 = (unsigned long long)(uint32_t)(uint64_t)(d >> 32);
-    unsigned long long l2 = (unsigned long long)(uint32_t)(uint64_t)(d >> 64);
-    unsigned long long l3 = (unsigned long long)(long long)(d >> 96);
-    if (l0) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_D0 + key), l0);
-    if (l1) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_D1 + key), l1);
-    if (l2) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_D2 + key), l2);
-    if (l3) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_D3 + key), l3);
-    if (s) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_S0 + key), (unsigned long long)s);
-    if (h) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_H0 + key), (unsigned long long)h);
-}
-
-// exact-binning HALF/SINGLE units of the scaled mantissas mx, my in [1,2)
-// (emulate.py:137-146 with u == e: sx = x 2^-ex, sy = y 2^-ey)
-__device__ __forceinline__ void exact_variants(double mx, double my, int32_t& ks, int32_t& kh) {
-    float rx = __double2float_rn(mx), ry = __double2float_rn(my);
-    uint32_t sb = __float_as_uint(__fmul_rn(rx, ry));                    // in [1, 4]
-    ks = (int32_t)(((sb & 0x7FFFFFu) | 0x800000u) << ((sb >> 23) - 127)); // units of 2^-23
-    __half hx = __double2half(mx), hy = __double2half(my);
-    uint32_t hb = __half_as_ushort(__hmul(hx, hy));                       // in [1, 4]
-    kh = (int32_t)(((hb & 0x3FFu) | 0x400u) << ((hb >> 10) - 15));        // units of 2^-10
-}
-
-__device__ __forceinline__ void cold_add(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B,
-                                         int key, int64_t kd, int32_t ks, int32_t kh) {
-    int c = key - S.cbase;
-    if ((unsigned)c < (unsigned)P1_CW) {
-        atomicAdd(&S.c_cnt[c], 1ull);
-        atomicAdd(&S.c_dlo[c], (unsigned long long)(uint32_t)(uint64_t)kd);
-        atomicAdd(&S.c_dhi[c], (unsigned long long)(kd >> 32));
-        atomicAdd(&S.c_s[c], (unsigned long long)(long long)ks);
-        atomicAdd(&S.c_h[c], (unsigned long long)(long long)kh);
-    } else {
-        push_key(A, B, key, 1ull, (__int128)kd, ks, kh);
-    }
-}
-
-// zero / subnormal / non-finite / extreme-exponent elements
-__device__ __noinline__ void p1_slow(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B,
-                                     double xv, double yv, uint32_t& zc, uint32_t& nf) {
-    uint64_t bx = dbits(xv), by = dbits(yv);
-    if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) { nf++; return; }
-    if (xv == 0.0 || yv == 0.0) { zc++; return; }                      // floatbits.py:74
-    int e = flexp_bits(bx) + flexp_bits(by);
-    int key = e + KOFF;
-    double p = __dmul_rn(xv, yv);
-    uint64_t pb = dbits(p);
-    int64_t kd = 0;
-    if (((pb >> 52) & 0x7FF) == 0x7FF) {                               // DOUBLE product overflow
-        atomicAdd(reinterpret_cast<unsigned long long*>(B + ((pb >> 63) ? B_INFN : B_INFP) + key), 1ull);
-    } else {
-        kd = double_units(pb, e);
-    }
-    int32_t ks, kh;
-    exact_variants(bitsd(mant_bits(bx)), bitsd(mant_bits(by)), ks, kh);
-    int32_t sg = (int32_t)((bx ^ by) >> 63);
-    sg = -sg;
-    ks = (ks ^ sg) - sg;
-    kh = (kh ^ sg) - sg;
-    cold_add(S, A, B, key, kd, ks, kh);
-}
-
-__device__ __forceinline__ void p1_element(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B,
-                                           double xv, double yv, int tid, uint32_t& zc, uint32_t& nf) {
-    uint64_t bx = dbits(xv), by = dbits(yv);
-    uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
-    int e = (int)(fx + fy) - 2046;
-    bool fast = (fx - 1u < 0x7FEu) & (fy - 1u < 0x7FEu) & ((unsigned)(e + 1022) <= 2043u);
-    if (fast) {
-        // DOUBLE: fl(x*y) in units of 2^(e-52)  (emulate.py:133)
-        uint64_t pb = dbits(__dmul_rn(xv, yv));
-        uint64_t pm = (pb & 0xFFFFFFFFFFFFFull) | (1ull << 52);
-        int sh = (int)((pb >> 52) & 0x7FF) - 1023 - e;                   // 0..2
-        int64_t kd = (int64_t)(pm << sh);
-        int64_t sg = (int64_t)(bx ^ by) >> 63;                            // 0 / -1
-        kd = (kd ^ sg) - sg;
-        int32_t ks, kh;
-        exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
-                       bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
-        int32_t sg32 = (int32_t)sg;
-        ks = (ks ^ sg32) - sg32;
-        kh = (kh ^ sg32) - sg32;
-        int key = e + KOFF;
-        int rel = key - S.base;
-        if ((unsigned)rel < (unsigned)P1_W) {
-            long long inc = ((long long)ks << 29) + ((long long)kh << 8) + 1;
-            ulonglong2* slot = &S.priv[rel * P1_T + tid];
-            ulonglong2 v = *slot;
-            v.x += (unsigned long long)kd;
-            v.y += (unsigned long long)inc;
-            *slot = v;
-        } else {
-            cold_add(S, A, B, key, kd, ks, kh);
-        }
-    } else {
-        p1_slow(S, A, B, xv, yv, zc, nf);
-    }
-}
-
-// reduce the private slots into the CTA totals and clear them (all threads)
-__device__ __forceinline__ void p1_flush(P1Shared& S, int tid) {
-    __syncthreads();
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int r = warp; r < P1_W; r += P1_T / 32) {
-        uint64_t dlo = 0;
-        int64_t dhi = 0;
-        long long ss = 0, hs = 0, cs = 0;
-        for (int i = lane; i < P1_T; i += 32) {
-            ulonglong2 v = S.priv[r * P1_T + i];
-            S.priv[r * P1_T + i] = make_ulonglong2(0ull, 0ull);
-            int64_t d = (int64_t)v.x;
-            uint64_t nl = dlo + (uint64_t)d;
-            dhi += (d >> 63) + (nl < dlo ? 1 : 0);
-            dlo = nl;
-            long long w = (long long)v.y;
-            long long c = w & 0xFF;
-            long long w1 = (w - c) >> 8;
-            long long h = ((w1 & 0x1FFFFF) ^ 0x100000) - 0x100000;
-            long long s = (w1 - h) >> 21;
-            cs += c; hs += h; ss += s;
-        }
-        for (int o = 16; o; o >>= 1) {
-            uint64_t olo = __shfl_xor_sync(0xffffffffu, dlo, o);
-            int64_t ohi = __shfl_xor_sync(0xffffffffu, dhi, o);
-            uint64_t nl = dlo + olo;
-            dhi += ohi + (nl < dlo ? 1 : 0);
-            dlo = nl;
-            ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            hs += __shfl_xor_sync(0xffffffffu, hs, o);
-            cs += __shfl_xor_sync(0xffffffffu, cs, o);
-        }
-        if (lane == 0) {
-            S.t_d[r] += ((__int128)dhi << 64) | (__int128)dlo;
-            S.t_s[r] += ss;
-            S.t_h[r] += hs;
-            S.t_c[r] += cs;
-        }
-    }
-    __syncthreads();
-}
-
-template <bool NORM, bool VEC>
-__device__ __forceinline__ void p1_load(const double* __restrict__ x, const double* __restrict__ y,
-                                        int64_t n, int64_t tile, int tid, double (&xv)[P1_EPT],
-                                        double (&yv)[P1_EPT], bool& full) {
-    const int64_t e0 = tile * P1_TILE;
-    full = e0 + P1_TILE <= n;
-    if (VEC && full) {
-        const double2* x2 = reinterpret_cast<const double2*>(x + e0);
-        const double2* y2 = reinterpret_cast<const double2*>(y + e0);
-#pragma unroll
-        for (int v = 0; v < P1_V; ++v) {
-            double2 a = __ldcs(x2 + v * P1_T + tid);
-            xv[2 * v] = a.x; xv[2 * v + 1] = a.y;
-            if (!NORM) {
-                double2 b = __ldcs(y2 + v * P1_T + tid);
-                yv[2 * v] = b.x; yv[2 * v + 1] = b.y;
-            }
-        }
-    } else {
-#pragma unroll
-        for (int v = 0; v < P1_V; ++v) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                int64_t i = e0 + 2 * ((int64_t)v * P1_T + tid) + k;
-                bool ok = i < n;
-                xv[2 * v + k] = ok ? __ldcs(x + i) : 0.0;
-                if (!NORM) yv[2 * v + k] = ok ? __ldcs(y + i) : 0.0;
-            }
-        }
-    }
-    if (NORM) {
-#pragma unroll
-        for (int j = 0; j < P1_EPT; ++j) yv[j] = xv[j];
-    }
-}
-
-template <bool NORM, bool VEC>
-__global__ void __launch_bounds__(P1_T, 3)
-k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-        int64_t* __restrict__ A, int64_t* __restrict__ B) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    P1Shared& S = *reinterpret_cast<P1Shared*>(smem_raw);
-    const int tid = threadIdx.x;
-    const int64_t ntiles = (n + P1_TILE - 1) / P1_TILE;
-
-    // ---- choose the private window from this CTA's first tile: the P1_W
-    // consecutive keys holding most sampled elements (sliding-window argmax).
-    uint32_t* hist = reinterpret_cast<uint32_t*>(S.priv);           // KEYS u32 (reuses priv)
-    uint32_t* pref = hist + 4224;                                   // KEYS+1 u32
-    for (int k = tid; k < 4224 * 2; k += P1_T) hist[k] = 0u;
-    __syncthreads();
-    if ((int64_t)blockIdx.x < ntiles) {
-        double xv[P1_EPT], yv[P1_EPT];
-        bool full;
-        p1_load<NORM, VEC>(x, y, n, blockIdx.x, tid, xv, yv, full);
-        const int64_t e0 = (int64_t)blockIdx.x * P1_TILE;
-#pragma unroll
-        for (int j = 0; j < P1_EPT; ++j) {
-            int64_t i = e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1);
-            if (i >= n) continue;
-            uint64_t bx = dbits(xv[j]), by = dbits(yv[j]);
-            uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
-            if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) atomicAdd(&hist[(int)(fx + fy) - 2046 + KOFF], 1u);
-        }
-    }
-    __syncthreads();
-    {   // inclusive prefix over KEYS (17 keys per thread)
-        constexpr int PER = (KEYS + P1_T - 1) / P1_T;
-        uint32_t loc[PER];
-        uint32_t run = 0;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            int k = tid * PER + i;
-            run += k < KEYS ? hist[k] : 0u;
-            loc[i] = run;
-        }
-        // block exclusive scan of per-thread totals
-        const int lane = tid & 31, warp = tid >> 5;
-        uint32_t incl = run;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) S.red[warp] = incl;
-        __syncthreads();
-        uint32_t wpre = 0;
-        for (int w = 0; w < warp; ++w) wpre += (uint32_t)S.red[w];
-        uint32_t pre = wpre + incl - run;
-        pref[0] = 0u;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            int k = tid * PER + i;
-            if (k < KEYS) pref[k + 1] = pre + loc[i];
-        }
-    }
-    __syncthreads();
-    {   // argmax over window starts b: sum = pref[b+W] - pref[b]
-        unsigned long long best = 0ull;
-        for (int b = tid; b + P1_W <= KEYS; b += P1_T) {
-            uint32_t s = pref[b + P1_W] - pref[b];
-            unsigned long long cand = ((unsigned long long)s << 32) | (uint32_t)(0xFFFFFFFFu - b);
-            best = cand > best ? cand : best;
-        }
-        for (int o = 16; o; o >>= 1) {
-            unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
-            best = t > best ? t : best;
-        }
-        __syncthreads();
-        if ((tid & 31) == 0) S.red[tid >> 5] = best;
-        __syncthreads();
-        if (tid == 0) {
-            unsigned long long m = 0ull;
-            for (int w = 0; w < P1_T / 32; ++w) m = S.red[w] > m ? S.red[w] : m;
-            int b = (m >> 32) ? (int)(0xFFFFFFFFu - (uint32_t)m) : (KOFF - 8);   // default near e = 0
-            S.base = b;
-            int cb = b - (P1_CW - P1_W) / 2;
-            cb = cb < 0 ? 0 : cb;
-            cb = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
-            S.cbase = cb;
-        }
-    }
-    __syncthreads();
-    // ---- clear private slots, cold table and totals
-    for (int k = tid; k < P1_W * P1_T; k += P1_T) S.priv[k] = make_ulonglong2(0ull, 0ull);
-    for (int k = tid; k < P1_CW; k += P1_T) {
-        S.c_cnt[k] = 0ull; S.c_dlo[k] = 0ull; S.c_dhi[k] = 0ull; S.c_s[k] = 0ull; S.c_h[k] = 0ull;
-    }
-    if (tid < P1_W) { S.t_d[tid] = 0; S.t_s[tid] = 0; S.t_h[tid] = 0; S.t_c[tid] = 0; }
-    __syncthreads();
-
-    // ---- main streaming loop (persistent grid over tiles)
-    uint32_t zc = 0, nf = 0;
-    int since = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        double xv[P1_EPT], yv[P1_EPT];
-        bool full;
-        p1_load<NORM, VEC>(x, y, n, t, tid, xv, yv, full);
-        if (full) {
-#pragma unroll
-            for (int j = 0; j < P1_EPT; ++j) p1_element(S, A, B, xv[j], yv[j], tid, zc, nf);
-        } else {
-            const int64_t e0 = t * P1_TILE;
-#pragma unroll
-            for (int j = 0; j < P1_EPT; ++j) {
-                int64_t i = e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1);
-                if (i < n) p1_element(S, A, B, xv[j], yv[j], tid, zc, nf);
-            }
-        }
-        if (++since == P1_FLUSH) { p1_flush(S, tid); since = 0; }
-    }
-    p1_flush(S, tid);
-
-    // ---- publish CTA partials
-    for (int r = tid; r < P1_W; r += P1_T)
-        if (S.t_c[r]) push_key(A, B, S.base + r, (unsigned long long)S.t_c[r], S.t_d[r], S.t_s[r], S.t_h[r]);
-    for (int c = tid; c < P1_CW; c += P1_T) {
-        if (S.c_cnt[c]) {
-            __int128 d = ((__int128)(long long)S.c_dhi[c] << 32) + (__int128)S.c_dlo[c];
-            push_key(A, B, S.cbase + c, S.c_cnt[c], d, (long long)S.c_s[c], (long long)S.c_h[c]);
-        }
-    }
-    // zero / non-finite counts
-    unsigned long long z = zc, f = nf;
-    for (int o = 16; o; o >>= 1) {
-        z += __shfl_xor_sync(0xffffffffu, z, o);
-        f += __shfl_xor_sync(0xffffffffu, f, o);
-    }
-    if ((tid & 31) == 0) {
-        if (z) atomicAdd(reinterpret_cast<unsigned long long*>(A + A_ZERO), z);
-        if (f) atomicAdd(reinterpret_cast<unsigned long long*>(A + A_NONFINITE), f);
-    }
-}
+#include "qdot_pass1.cuh"
 
 // =============================================================================
 // score (one CTA)
@@ -648,7 +306,8 @@ k_score(const int64_t* __restrict__ A, int32_t* __restrict__ lut_bin, uint32_t* 
         if (b >= 0) {
             int pr = bins[b].precision;
             long long delta = bins[b].upper - (long long)(k - KOFF);
-            if ((pr == QDOT_HALF || pr == QDOT_SINGLE) && delta > 0 && S.s_status == QDOT_OK) {
+            if ((pr == QDOT_HALF || pr == QDOT_SINGLE) && (delta > 0 || A[A_HOT + k] > 0) &&
+                S.s_status == QDOT_OK) {
                 d = P2_NEED | (pr == QDOT_HALF ? P2_HALF : 0u) |
                     (uint32_t)(delta > P2_DELTA_MAX ? P2_DELTA_MAX : delta);
                 need = 1;
@@ -769,8 +428,8 @@ __device__ __forceinline__ __int128 key_double(const int64_t* __restrict__ B, in
 }
 
 __global__ void __launch_bounds__(FN_T, 1)
-k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const ScoreMeta* __restrict__ meta,
-           qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
+k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const uint32_t* __restrict__ lut_p2,
+           const ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
     __shared__ int s_ovf, s_half;
     const int tid = threadIdx.x;
     const ScoreMeta m = *meta;
@@ -815,7 +474,7 @@ k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const S
                 long long c = A[A_CNT + k];
                 if (!c) continue;
                 long long d = u - (long long)(k - KOFF);
-                long long v = d == 0 ? (half ? B[B_H0 + k] : B[B_S0 + k]) : B[B_P2 + k];
+                long long v = (lut_p2[k] & P2_NEED) ? B[B_P2 + k] : (half ? B[B_H0 + k] : B[B_S0 + k]);
                 acc.add((__int128)v, qs_of(k));
                 mass += (double)c * ldexp(4.0, (int)(d > 2000 ? -2000 : -d));
             }
@@ -896,10 +555,10 @@ static int occupancy(K kern, int threads, size_t smem) {
     return occ > 0 ? occ : 1;
 }
 
-template <bool NORM, bool VEC>
+template <bool NORM, bool VEC, int V, bool PF>
 static cudaError_t launch_pass1_t(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
-                                  cudaStream_t st) {
-    auto kern = k_pass1<NORM, VEC>;
+                                  const P1Params& prm, cudaStream_t st) {
+    auto kern = k_pass1<NORM, VEC, V, PF>;
     const size_t smem = sizeof(P1Shared);
     static bool attr = false;
     if (!attr) {
@@ -908,20 +567,44 @@ static cudaError_t launch_pass1_t(const double* x, const double* y, int64_t n, i
     }
     static int occ = 0;
     if (!occ) occ = occupancy(kern, P1_T, smem);
-    int64_t ntiles = (n + P1_TILE - 1) / P1_TILE;
+    const int64_t tile = (int64_t)P1_T * 2 * V;
+    int64_t ntiles = (n + tile - 1) / tile;
     int64_t grid = (int64_t)sm_count_cached() * occ;
     if (grid > ntiles) grid = ntiles;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, P1_T, smem, st>>>(x, y, n, A, B);
+    kern<<<(unsigned)grid, P1_T, smem, st>>>(x, y, n, A, B, prm);
     return cudaGetLastError();
 }
 
+// pass-1 variant (vector width / prefetch); QDOT_B200_P1_VARIANT overrides for tuning
+static int p1_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("QDOT_B200_P1_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <bool NORM, bool VEC>
+static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
+                                  const P1Params& prm, cudaStream_t st) {
+    switch (p1_variant()) {
+        case 1: return launch_pass1_t<NORM, VEC, 2, false>(x, y, n, A, B, prm, st);
+        case 2: return launch_pass1_t<NORM, VEC, 2, true>(x, y, n, A, B, prm, st);
+        case 3: return launch_pass1_t<NORM, VEC, 4, true>(x, y, n, A, B, prm, st);
+        default: return launch_pass1_t<NORM, VEC, 4, false>(x, y, n, A, B, prm, st);
+    }
+}
+
 cudaError_t launch_pass1(const double* x, const double* y, int64_t n, bool norm, int64_t* A, int64_t* B,
-                         cudaStream_t st) {
+                         const P1Params& prm, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     bool vec = ((reinterpret_cast<uintptr_t>(x) | (norm ? 0 : reinterpret_cast<uintptr_t>(y))) & 15u) == 0;
-    if (norm) return vec ? launch_pass1_t<true, true>(x, x, n, A, B, st) : launch_pass1_t<true, false>(x, x, n, A, B, st);
-    return vec ? launch_pass1_t<false, true>(x, y, n, A, B, st) : launch_pass1_t<false, false>(x, y, n, A, B, st);
+    if (norm) return vec ? launch_pass1_v<true, true>(x, x, n, A, B, prm, st)
+                         : launch_pass1_v<true, false>(x, x, n, A, B, prm, st);
+    return vec ? launch_pass1_v<false, true>(x, y, n, A, B, prm, st)
+               : launch_pass1_v<false, false>(x, y, n, A, B, prm, st);
 }
 
 cudaError_t launch_score(const int64_t* A, int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta,
@@ -967,9 +650,9 @@ cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm,
                : launch_pass2_t<false, false>(x, y, n, lut_p2, meta, B, st);
 }
 
-cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const ScoreMeta* meta, qdot_result* res,
-                            qdot_bin* bins, cudaStream_t st) {
-    k_finalize<<<1, FN_T, 0, st>>>(A, B, meta, res, bins);
+cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
+                            qdot_result* res, qdot_bin* bins, cudaStream_t st) {
+    k_finalize<<<1, FN_T, 0, st>>>(A, B, lut_p2, meta, res, bins);
     return cudaGetLastError();
 }
 

@@ -12,14 +12,14 @@ size_t score_smem_bytes();
 size_t pass2_smem_bytes();
 
 cudaError_t launch_pass1(const double* x, const double* y, int64_t n, bool norm, int64_t* A, int64_t* B,
-                         cudaStream_t st);
+                         const P1Params& prm, cudaStream_t st);
 cudaError_t launch_score(const int64_t* A, int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta,
                          qdot_result* res, qdot_bin* bins, int64_t n_total, const qdot_config& cfg,
                          cudaStream_t st);
 cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm, const uint32_t* lut_p2,
                          const ScoreMeta* meta, int64_t* B, cudaStream_t st);
-cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const ScoreMeta* meta, qdot_result* res,
-                            qdot_bin* bins, cudaStream_t st);
+cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
+                            qdot_result* res, qdot_bin* bins, cudaStream_t st);
 cudaError_t launch_bin_ids(const double* x, const double* y, int64_t n, bool norm, const int32_t* lut_bin,
                            int32_t* out, cudaStream_t st);
 

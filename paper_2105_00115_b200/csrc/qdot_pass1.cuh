@@ -1,0 +1,465 @@
+// qdot_pass1.cuh -- the streaming pass (included into namespace qd of qdot_kernels.cu).
+//
+// Per element (floatbits.py:57-93 + emulate.py:133-146):
+//   key  = flexp(x) + flexp(y) + 2148        exponent-sum histogram bin
+//   D    = fl(x*y) in units of 2^(e-52)      exact DOUBLE partial  (|D| <= 2^54)
+//   S0,H0 = exact-binning SINGLE / HALF products of the scaled mantissas in
+//          units of 2^-23 / 2^-10 (always for cold keys, for private-window
+//          keys only in full mode)
+//
+// Accumulation (all integer, order independent):
+//   * private window: P1_W consecutive keys chosen per CTA from a sample of
+//     its first tile; one 16-byte slot per (key, thread) in shared memory,
+//     updated with plain LDS/STS (no atomics);
+//   * cold window: P1_CW keys around it, per-CTA shared-memory tables of
+//     32-bit limbs updated with native 32-bit shared atomics;
+//   * anything else: global atomics.
+//   Both shared tables are flushed (private -> per-CTA totals, cold -> global)
+//   every <= 255 (full) / 511 (lean) elements per thread, which bounds every
+//   per-thread int64 and per-CTA 32-bit limb sum.
+//   Zero / subnormal / non-finite / extreme-exponent elements take a separate
+//   non-inlined path.
+//
+// Lean vs full: the exact HALF/SINGLE variants are only needed for bins that
+// end up HALF or SINGLE.  Each CTA predicts from its sample (estimated bin
+// cardinality, exponent distance to the sampled maximum, epsilon) whether any
+// key of its private window can score in [0, 23); if not it runs the lean
+// loop (count + DOUBLE units only) and flags its window keys in A[A_HOT].
+// The score kernel sends flagged keys that did become HALF/SINGLE to pass 2,
+// so the prediction only affects speed, never results.
+
+constexpr int P1_T = 256;                    // threads per CTA
+constexpr int P1_W = 16;                     // keys with per-thread private slots
+constexpr int P1_CW = 128;                   // keys with per-CTA 32-bit limb tables
+// private window keys keep e in [-1022, 1021] (fl(x*y) normal and finite)
+constexpr int P1_SAFE_LO = KOFF - 1022;
+constexpr int P1_SAFE_HI = KOFF + 1021 - P1_W + 1;
+
+struct __align__(16) P1Shared {
+    ulonglong2 priv[P1_W * P1_T];            // lean: {D, count}; full: {D, packed S|H|count}
+    __int128 t_d[P1_W];                      // CTA totals of the private window
+    long long t_s[P1_W], t_h[P1_W], t_c[P1_W];
+    // cold window, 32-bit limbs: D = d0 + d1 2^14 + d2 2^28 + d3 2^42 (d3 signed),
+    // S = s0 + s1 2^14 (s1 signed), H (signed)
+    uint32_t c_cnt[P1_CW], c_d0[P1_CW], c_d1[P1_CW], c_d2[P1_CW], c_d3[P1_CW];
+    uint32_t c_s0[P1_CW], c_s1[P1_CW], c_h[P1_CW];
+    unsigned long long red[2 * (P1_T / 32)];
+    int base;                                // first key of the private window
+    int cbase;                               // first key of the cold window
+    int full;                                // this CTA runs the full-variant loop
+    int kmax;                                // largest sampled key
+};
+
+size_t pass1_smem_bytes() { return sizeof(P1Shared); }
+
+// push one key's exact partials to the global tables (region A / B)
+__device__ __forceinline__ void push_key(int64_t* __restrict__ A, int64_t* __restrict__ B, int key,
+                                         unsigned long long cnt, __int128 d, long long s, long long h) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(A + A_CNT + key), cnt);
+    unsigned long long l0 = (unsigned long long)(uint32_t)(uint64_t)d;
+    unsigned long long l1 = (unsigned long long)(uint32_t)(uint64_t)(d >> 32);
+    unsigned long long l2 = (unsigned long long)(uint32_t)(uint64_t)(d >> 64);
+    unsigned long long l3 = (unsigned long long)(long long)(d >> 96);
+    if (l0) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_D0 + key), l0);
+    if (l1) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_D1 + key), l1);
+    if (l2) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_D2 + key), l2);
+    if (l3) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_D3 + key), l3);
+    if (s) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_S0 + key), (unsigned long long)s);
+    if (h) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_H0 + key), (unsigned long long)h);
+}
+
+// exact-binning HALF/SINGLE units of the scaled mantissas mx, my in [1,2)
+// (emulate.py:137-146 with u == e: sx = x 2^-ex, sy = y 2^-ey)
+__device__ __forceinline__ void exact_variants(double mx, double my, int32_t& ks, int32_t& kh) {
+    float rx = __double2float_rn(mx), ry = __double2float_rn(my);
+    uint32_t sb = __float_as_uint(__fmul_rn(rx, ry));                    // in [1, 4]
+    ks = (int32_t)(((sb & 0x7FFFFFu) | 0x800000u) << ((sb >> 23) - 127)); // units of 2^-23
+    __half hx = __double2half(mx), hy = __double2half(my);
+    uint32_t hb = __half_as_ushort(__hmul(hx, hy));                       // in [1, 4]
+    kh = (int32_t)(((hb & 0x3FFu) | 0x400u) << ((hb >> 10) - 15));        // units of 2^-10
+}
+
+// cold key: variants from the mantissa bits (mbx, mby = raw bits of mx, my),
+// then the per-CTA limb table or, outside it, global atomics
+__device__ __forceinline__ void p1_cold(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B, int key,
+                                        int64_t kd, uint64_t mbx, uint64_t mby, int32_t sg) {
+    int32_t ks, kh;
+    exact_variants(bitsd(mbx), bitsd(mby), ks, kh);
+    ks = (ks ^ sg) - sg;
+    kh = (kh ^ sg) - sg;
+    int c = key - S.cbase;
+    if ((unsigned)c < (unsigned)P1_CW) {
+        uint64_t u = (uint64_t)kd;
+        atomicAdd(&S.c_cnt[c], 1u);
+        atomicAdd(&S.c_d0[c], (uint32_t)(u & 0x3FFFu));
+        atomicAdd(&S.c_d1[c], (uint32_t)((u >> 14) & 0x3FFFu));
+        atomicAdd(&S.c_d2[c], (uint32_t)((u >> 28) & 0x3FFFu));
+        atomicAdd(&S.c_d3[c], (uint32_t)(int32_t)(kd >> 42));
+        atomicAdd(&S.c_s0[c], (uint32_t)ks & 0x3FFFu);
+        atomicAdd(&S.c_s1[c], (uint32_t)(ks >> 14));
+        atomicAdd(&S.c_h[c], (uint32_t)kh);
+    } else {
+        push_key(A, B, key, 1ull, (__int128)kd, ks, kh);
+    }
+}
+
+// zero / subnormal / non-finite / extreme-exponent elements
+__device__ __noinline__ void p1_special(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B,
+                                        double xv, double yv, uint32_t* zc, uint32_t* nf) {
+    uint64_t bx = dbits(xv), by = dbits(yv);
+    if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) { (*nf)++; return; }
+    if (xv == 0.0 || yv == 0.0) { (*zc)++; return; }                   // floatbits.py:74
+    int e = flexp_bits(bx) + flexp_bits(by);
+    int key = e + KOFF;
+    uint64_t pb = dbits(__dmul_rn(xv, yv));
+    int64_t kd = 0;
+    if (((pb >> 52) & 0x7FF) == 0x7FF) {                               // DOUBLE product overflow
+        atomicAdd(reinterpret_cast<unsigned long long*>(B + ((pb >> 63) ? B_INFN : B_INFP) + key), 1ull);
+    } else {
+        kd = double_units(pb, e);
+    }
+    p1_cold(S, A, B, key, kd, mant_bits(bx), mant_bits(by), -(int32_t)((bx ^ by) >> 63));
+}
+
+// one element
+template <bool FULL>
+__device__ __forceinline__ void p1_elem(P1Shared& S, ulonglong2* __restrict__ my, int kbias,
+                                        int64_t* __restrict__ A, int64_t* __restrict__ B, double xv, double yv,
+                                        uint32_t* zc, uint32_t* nf) {
+    uint64_t bx = dbits(xv), by = dbits(yv);
+    uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
+    uint32_t esum = fx + fy;                                            // e + 2046
+    bool normal = (fx - 1u < 0x7FEu) & (fy - 1u < 0x7FEu) & (esum - 1024u < 2044u);   // e in [-1022, 1021]
+    if (normal) {
+        // DOUBLE: fl(x*y) in units of 2^(e-52)  (emulate.py:133)
+        uint64_t pb = dbits(__dmul_rn(xv, yv));
+        uint64_t pm = (pb & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+        int sh = (int)((uint32_t)(pb >> 52) & 0x7FFu) + 1023 - (int)esum;          // 0..2
+        int64_t kd = (int64_t)(pm << sh);
+        int64_t sg = (int64_t)((int32_t)(uint32_t)(pb >> 32) >> 31);             // 0 / -1
+        kd = (kd ^ sg) - sg;
+        const int rel = (int)esum + kbias;                                        // key - base
+        if ((unsigned)rel < (unsigned)P1_W) {
+            ulonglong2* slot = my + rel * P1_T;
+            ulonglong2 v = *slot;
+            v.x += (unsigned long long)kd;
+            if (FULL) {
+                int32_t ks, kh;
+                exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
+                               bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
+                int32_t s32 = (int32_t)sg;
+                ks = (ks ^ s32) - s32;
+                kh = (kh ^ s32) - s32;
+                v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
+            } else {
+                v.y += 1ull;
+            }
+            *slot = v;
+        } else {
+            p1_cold(S, A, B, (int)esum - 2046 + KOFF, kd, (bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull,
+                    (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)sg);
+        }
+    } else {
+        p1_special(S, A, B, xv, yv, zc, nf);
+    }
+}
+
+// reduce the private slots into the CTA totals, push the cold table to the
+// global tables, clear both (all threads of the CTA)
+template <bool FULL>
+__device__ __forceinline__ void p1_flush(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B, int tid) {
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int r = warp; r < P1_W; r += P1_T / 32) {
+        uint64_t dlo = 0;
+        int64_t dhi = 0;
+        long long ss = 0, hs = 0, cs = 0;
+        for (int i = lane; i < P1_T; i += 32) {
+            ulonglong2 v = S.priv[r * P1_T + i];
+            S.priv[r * P1_T + i] = make_ulonglong2(0ull, 0ull);
+            int64_t d = (int64_t)v.x;
+            uint64_t nl = dlo + (uint64_t)d;
+            dhi += (d >> 63) + (nl < dlo ? 1 : 0);
+            dlo = nl;
+            if (FULL) {
+                long long w = (long long)v.y;
+                long long c = w & 0xFF;
+                long long w1 = (w - c) >> 8;
+                long long h = ((w1 & 0x1FFFFF) ^ 0x100000) - 0x100000;
+                long long s = (w1 - h) >> 21;
+                cs += c; hs += h; ss += s;
+            } else {
+                cs += (long long)v.y;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            uint64_t olo = __shfl_xor_sync(0xffffffffu, dlo, o);
+            int64_t ohi = __shfl_xor_sync(0xffffffffu, dhi, o);
+            uint64_t nl = dlo + olo;
+            dhi += ohi + (nl < dlo ? 1 : 0);
+            dlo = nl;
+            cs += __shfl_xor_sync(0xffffffffu, cs, o);
+            if (FULL) {
+                ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                hs += __shfl_xor_sync(0xffffffffu, hs, o);
+            }
+        }
+        if (lane == 0) {
+            S.t_d[r] += ((__int128)dhi << 64) | (__int128)dlo;
+            S.t_s[r] += ss;
+            S.t_h[r] += hs;
+            S.t_c[r] += cs;
+        }
+    }
+    for (int c = tid; c < P1_CW; c += P1_T) {
+        uint32_t cnt = S.c_cnt[c];
+        if (cnt) {
+            __int128 d = (__int128)S.c_d0[c] + ((__int128)S.c_d1[c] << 14) + ((__int128)S.c_d2[c] << 28) +
+                         ((__int128)(int32_t)S.c_d3[c] << 42);
+            long long s = (long long)S.c_s0[c] + ((long long)(int32_t)S.c_s1[c] << 14);
+            push_key(A, B, S.cbase + c, cnt, d, s, (long long)(int32_t)S.c_h[c]);
+            S.c_cnt[c] = 0u; S.c_d0[c] = 0u; S.c_d1[c] = 0u; S.c_d2[c] = 0u; S.c_d3[c] = 0u;
+            S.c_s0[c] = 0u; S.c_s1[c] = 0u; S.c_h[c] = 0u;
+        }
+    }
+    __syncthreads();
+}
+
+template <bool NORM, bool VEC, int V>
+__device__ __forceinline__ void p1_load(const double* __restrict__ x, const double* __restrict__ y,
+                                        int64_t n, int64_t tile, int tid, double (&xv)[2 * V],
+                                        double (&yv)[2 * V], bool& full) {
+    constexpr int TILE = P1_T * 2 * V;
+    const int64_t e0 = tile * TILE;
+    full = e0 + TILE <= n;
+    if (VEC && full) {
+        const double2* x2 = reinterpret_cast<const double2*>(x + e0);
+        const double2* y2 = reinterpret_cast<const double2*>(y + e0);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            double2 a = __ldcs(x2 + v * P1_T + tid);
+            xv[2 * v] = a.x; xv[2 * v + 1] = a.y;
+            if (!NORM) {
+                double2 b = __ldcs(y2 + v * P1_T + tid);
+                yv[2 * v] = b.x; yv[2 * v + 1] = b.y;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                int64_t i = e0 + 2 * ((int64_t)v * P1_T + tid) + k;
+                bool ok = i < n;
+                xv[2 * v + k] = ok ? __ldcs(x + i) : 0.0;
+                if (!NORM) yv[2 * v + k] = ok ? __ldcs(y + i) : 0.0;
+            }
+        }
+    }
+    if (NORM) {
+#pragma unroll
+        for (int j = 0; j < 2 * V; ++j) yv[j] = xv[j];
+    }
+}
+
+template <bool FULL, int V>
+__device__ __forceinline__ void p1_tile(P1Shared& S, ulonglong2* __restrict__ my, int kbias,
+                                        int64_t* __restrict__ A, int64_t* __restrict__ B,
+                                        const double (&xv)[2 * V], const double (&yv)[2 * V], int64_t e0,
+                                        int64_t n, bool fulltile, int tid, uint32_t* zc, uint32_t* nf) {
+#pragma unroll
+    for (int j = 0; j < 2 * V; ++j) {
+        if (fulltile || (e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1) < n))
+            p1_elem<FULL>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+    }
+}
+
+// persistent loop over tiles.  PF: register double buffering (the loads of
+// the CTA's next tile are in flight while the current one is processed).
+template <bool NORM, bool VEC, bool FULL, int V, bool PF>
+__device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ x, const double* __restrict__ y,
+                                        int64_t n, int64_t* __restrict__ A, int64_t* __restrict__ B, int tid,
+                                        uint32_t* zc, uint32_t* nf) {
+    constexpr int EPT = 2 * V;
+    constexpr int TILE = P1_T * EPT;
+    constexpr int FLUSH = (FULL ? 255 : 511) / EPT;   // tiles between flushes
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    const int64_t stride = gridDim.x;
+    const int kbias = KOFF - 2046 - S.base;
+    ulonglong2* __restrict__ my = S.priv + tid;
+    int since = 0;
+    if (!PF) {
+        for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
+            double xv[EPT], yv[EPT];
+            bool f;
+            p1_load<NORM, VEC, V>(x, y, n, t, tid, xv, yv, f);
+            p1_tile<FULL, V>(S, my, kbias, A, B, xv, yv, t * TILE, n, f, tid, zc, nf);
+            if (++since == FLUSH) { p1_flush<FULL>(S, A, B, tid); since = 0; }
+        }
+    } else {
+        double xa[EPT], ya[EPT], xb[EPT], yb[EPT];
+        bool fa = false, fb = false;
+        int64_t t = blockIdx.x;
+        if (t < ntiles) p1_load<NORM, VEC, V>(x, y, n, t, tid, xa, ya, fa);
+        while (t < ntiles) {
+            const int64_t tb = t + stride;
+            if (tb < ntiles) p1_load<NORM, VEC, V>(x, y, n, tb, tid, xb, yb, fb);
+            p1_tile<FULL, V>(S, my, kbias, A, B, xa, ya, t * TILE, n, fa, tid, zc, nf);
+            if (++since == FLUSH) { p1_flush<FULL>(S, A, B, tid); since = 0; }
+            if (tb >= ntiles) break;
+            const int64_t ta = tb + stride;
+            if (ta < ntiles) p1_load<NORM, VEC, V>(x, y, n, ta, tid, xa, ya, fa);
+            p1_tile<FULL, V>(S, my, kbias, A, B, xb, yb, tb * TILE, n, fb, tid, zc, nf);
+            if (++since == FLUSH) { p1_flush<FULL>(S, A, B, tid); since = 0; }
+            t = ta;
+        }
+    }
+    p1_flush<FULL>(S, A, B, tid);
+}
+
+template <bool NORM, bool VEC, int V, bool PF>
+__global__ void __launch_bounds__(P1_T, 3)
+k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+        int64_t* __restrict__ A, int64_t* __restrict__ B, P1Params prm) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    P1Shared& S = *reinterpret_cast<P1Shared*>(smem_raw);
+    const int tid = threadIdx.x;
+    constexpr int TILE = P1_T * 2 * V;
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+
+    // ---- sample this CTA's first tile: histogram of keys (reusing priv)
+    uint32_t* hist = reinterpret_cast<uint32_t*>(S.priv);           // KEYS u32
+    uint32_t* pref = hist + 4224;                                   // KEYS+1 u32
+    for (int k = tid; k < 4224 * 2; k += P1_T) hist[k] = 0u;
+    __syncthreads();
+    if ((int64_t)blockIdx.x < ntiles) {
+        double xv[2 * V], yv[2 * V];
+        bool full;
+        p1_load<NORM, VEC, V>(x, y, n, blockIdx.x, tid, xv, yv, full);
+        const int64_t e0 = (int64_t)blockIdx.x * TILE;
+#pragma unroll
+        for (int j = 0; j < 2 * V; ++j) {
+            int64_t i = e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1);
+            if (i >= n) continue;
+            uint64_t bx = dbits(xv[j]), by = dbits(yv[j]);
+            uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
+            if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) atomicAdd(&hist[(int)(fx + fy) - 2046 + KOFF], 1u);
+        }
+    }
+    __syncthreads();
+    {   // inclusive prefix over KEYS (17 keys per thread) + largest sampled key
+        constexpr int PER = (KEYS + P1_T - 1) / P1_T;
+        uint32_t loc[PER];
+        uint32_t run = 0;
+        int kmx = -1;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            int k = tid * PER + i;
+            uint32_t h = k < KEYS ? hist[k] : 0u;
+            if (h) kmx = k;
+            run += h;
+            loc[i] = run;
+        }
+        const int lane = tid & 31, warp = tid >> 5;
+        uint32_t incl = run;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        for (int o = 16; o; o >>= 1) kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+        if (lane == 31) S.red[warp] = incl;
+        if (lane == 0) S.red[P1_T / 32 + warp] = (unsigned long long)(long long)kmx;
+        __syncthreads();
+        uint32_t wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += (uint32_t)S.red[w];
+        uint32_t pre = wpre + incl - run;
+        pref[0] = 0u;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            int k = tid * PER + i;
+            if (k < KEYS) pref[k + 1] = pre + loc[i];
+        }
+        if (tid == 0) {
+            int m = -1;
+            for (int w = 0; w < P1_T / 32; ++w) m = max(m, (int)(long long)S.red[P1_T / 32 + w]);
+            S.kmax = m;
+        }
+    }
+    __syncthreads();
+    {   // private window: argmax over starts b of pref[b+W] - pref[b], inside the safe range
+        unsigned long long best = 0ull;
+        for (int b = P1_SAFE_LO + tid; b <= P1_SAFE_HI; b += P1_T) {
+            uint32_t s = pref[b + P1_W] - pref[b];
+            unsigned long long cand = ((unsigned long long)s << 32) | (uint32_t)(0xFFFFFFFFu - b);
+            best = cand > best ? cand : best;
+        }
+        for (int o = 16; o; o >>= 1) {
+            unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+            best = t > best ? t : best;
+        }
+        __syncthreads();
+        if ((tid & 31) == 0) S.red[tid >> 5] = best;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long m = 0ull;
+            for (int w = 0; w < P1_T / 32; ++w) m = S.red[w] > m ? S.red[w] : m;
+            int b = (m >> 32) ? (int)(0xFFFFFFFFu - (uint32_t)m) : (KOFF - 8);   // default near e = 0
+            S.base = b;
+            int cb = b - (P1_CW - P1_W) / 2;
+            cb = cb < 0 ? 0 : cb;
+            cb = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
+            S.cbase = cb;
+            // lean / full decision (see header); only speed depends on it
+            int full = 0;
+            if (prm.mode == 2 || prm.input_mu != 52) full = 1;
+            else if (prm.mode == 0) {
+                const uint32_t ns = pref[KEYS];
+                const int fl = flexp_bits(dbits(prm.epsilon));
+                for (int r = 0; r < P1_W && ns; ++r) {
+                    uint32_t c = hist[b + r];
+                    if (!c) continue;
+                    double mest = (double)c * (double)prm.n_total / (double)ns;
+                    int lg = mest >= 1.0 ? flexp_bits(dbits(mest)) : 0;
+                    int score = lg - 2 + (b + r - S.kmax) - fl + 1;
+                    if (score > -6 && score < 27) full = 1;
+                }
+            }
+            S.full = full;
+        }
+    }
+    __syncthreads();
+    // ---- clear private slots, cold table and totals
+    for (int k = tid; k < P1_W * P1_T; k += P1_T) S.priv[k] = make_ulonglong2(0ull, 0ull);
+    for (int k = tid; k < P1_CW; k += P1_T) {
+        S.c_cnt[k] = 0u; S.c_d0[k] = 0u; S.c_d1[k] = 0u; S.c_d2[k] = 0u; S.c_d3[k] = 0u;
+        S.c_s0[k] = 0u; S.c_s1[k] = 0u; S.c_h[k] = 0u;
+    }
+    if (tid < P1_W) { S.t_d[tid] = 0; S.t_s[tid] = 0; S.t_h[tid] = 0; S.t_c[tid] = 0; }
+    __syncthreads();
+
+    // ---- main streaming loop (persistent grid over tiles)
+    uint32_t zc = 0, nf = 0;
+    const bool fullmode = S.full != 0;
+    if (fullmode) p1_main<NORM, VEC, true, V, PF>(S, x, y, n, A, B, tid, &zc, &nf);
+    else p1_main<NORM, VEC, false, V, PF>(S, x, y, n, A, B, tid, &zc, &nf);
+
+    // ---- publish CTA partials (the cold table was pushed by the last flush)
+    for (int r = tid; r < P1_W; r += P1_T) {
+        if (S.t_c[r]) {
+            push_key(A, B, S.base + r, (unsigned long long)S.t_c[r], S.t_d[r], S.t_s[r], S.t_h[r]);
+            if (!fullmode) atomicAdd(reinterpret_cast<unsigned long long*>(A + A_HOT + S.base + r),
+                                     (unsigned long long)S.t_c[r]);
+        }
+    }
+    if (tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(A + (fullmode ? A_FULLCTAS : A_LEANCTAS)), 1ull);
+    // zero / non-finite counts
+    unsigned long long z = zc, f = nf;
+    for (int o = 16; o; o >>= 1) {
+        z += __shfl_xor_sync(0xffffffffu, z, o);
+        f += __shfl_xor_sync(0xffffffffu, f, o);
+    }
+    if ((tid & 31) == 0) {
+        if (z) atomicAdd(reinterpret_cast<unsigned long long*>(A + A_ZERO), z);
+        if (f) atomicAdd(reinterpret_cast<unsigned long long*>(A + A_NONFINITE), f);
+    }
+}

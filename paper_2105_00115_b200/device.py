@@ -7,6 +7,7 @@ all arithmetic on the vectors happens in lib/libqdot_b200.so.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from typing import Optional, Tuple
 
@@ -15,6 +16,10 @@ import numpy as np
 from . import _lib
 
 _tls = threading.local()
+
+# pass-1 lean/full choice: 0 = per-CTA auto (default), 1 = force lean, 2 = force
+# full variants.  Only speed depends on it (tests run all three).
+PASS1_MODE = int(os.environ.get("QDOT_B200_PASS1_MODE", "0"))
 
 
 def _torch():
@@ -108,4 +113,5 @@ def config_struct(cfg, strategy) -> _lib.QdotConfig:
     c.input_mu = int(cfg.input_mu)
     c.strategy = code
     c.strategy_param = param
+    c.reserved = PASS1_MODE
     return c

@@ -112,7 +112,7 @@ def run_device(xd, yd, n: int, norm: bool, cfg: ToleranceConfig, strategy, st=No
         if torch_stream is not None:
             st.ev[0].record(torch_stream)
     _lib.check(lib.qdot_b200_begin(ws, s), lib)
-    _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(norm), ws, s), lib)
+    _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(norm), ctypes.byref(c), n, ws, s), lib)
     _lib.check(lib.qdot_b200_score(ws, n, ctypes.byref(c), s), lib)
     if torch_stream is not None:
         st.ev[1].record(torch_stream)
@@ -171,7 +171,7 @@ def select_parameters(x, y, cfg: ToleranceConfig, strategy: Strategy = None) -> 
     s = stream_handle(xd.device)
     ws = st.ws_ptr
     _lib.check(lib.qdot_b200_begin(ws, s), lib)
-    _lib.check(lib.qdot_b200_pass1(xd.data_ptr(), yd.data_ptr(), n, int(is_norm), ws, s), lib)
+    _lib.check(lib.qdot_b200_pass1(xd.data_ptr(), yd.data_ptr(), n, int(is_norm), ctypes.byref(c), n, ws, s), lib)
     _lib.check(lib.qdot_b200_score(ws, n, ctypes.byref(c), s), lib)
     # finalize also fills the result header and per-bin values; cheap (1 CTA)
     _lib.check(lib.qdot_b200_pass2(xd.data_ptr(), yd.data_ptr(), n, int(is_norm), ws, s), lib)

@@ -81,8 +81,15 @@ def check_against_golden(case, rep):
 CASES = G.select(max_n=1 << 20)
 
 
+@pytest.fixture(params=[0, 1, 2], ids=["auto", "lean", "full"])
+def pass1_mode(request, monkeypatch):
+    from paper_2105_00115_b200 import device
+    monkeypatch.setattr(device, "PASS1_MODE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
-def test_golden_case(case):
+def test_golden_case(case, pass1_mode):
     x, y = G.inputs(case)
     cfg = cfg_of(case)
     yy = x if case["norm"] else y
@@ -98,7 +105,7 @@ def test_golden_case(case):
 
 @pytest.mark.parametrize("seed", range(12))
 @pytest.mark.parametrize("strategy", ["exact", "ranged:3", "split:4"])
-def test_random_against_oracle(seed, strategy):
+def test_random_against_oracle(seed, strategy, pass1_mode):
     rng = np.random.default_rng(100 + seed)
     n = int(rng.integers(1, 20000))
     t = int(rng.integers(0, 120))
@@ -198,13 +205,14 @@ def test_sharded_tables_sum_like_one_device():
     ranks = [ThreadState(dev), ThreadState(dev)]
     s = torch.cuda.current_stream().cuda_stream
     parts = [(0, cut), (cut, n)]
+    c = config_struct(cfg, Q.ExactBinning())
     for st, (a, b) in zip(ranks, parts):
         _lib.check(lib.qdot_b200_begin(st.ws_ptr, s))
-        _lib.check(lib.qdot_b200_pass1(xd[a:].data_ptr(), yd[a:].data_ptr(), b - a, 0, st.ws_ptr, s))
+        _lib.check(lib.qdot_b200_pass1(xd[a:].data_ptr(), yd[a:].data_ptr(), b - a, 0, ctypes.byref(c), n,
+                                       st.ws_ptr, s))
     ra = ranks[0].region_a() + ranks[1].region_a()          # "allreduce" of region A
     for st in ranks:
         st.region_a().copy_(ra)
-    c = config_struct(cfg, Q.ExactBinning())
     for st, (a, b) in zip(ranks, parts):
         _lib.check(lib.qdot_b200_score(st.ws_ptr, n, ctypes.byref(c), s))
         _lib.check(lib.qdot_b200_pass2(xd[a:].data_ptr(), yd[a:].data_ptr(), b - a, 0, st.ws_ptr, s))
