@@ -590,10 +590,9 @@ template <bool NORM, bool VEC>
 static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
                                   const P1Params& prm, cudaStream_t st) {
     switch (p1_variant()) {
-        case 1: return launch_pass1_t<NORM, VEC, 2, false>(x, y, n, A, B, prm, st);
+        case 1: return launch_pass1_t<NORM, VEC, 4, false>(x, y, n, A, B, prm, st);
         case 2: return launch_pass1_t<NORM, VEC, 2, true>(x, y, n, A, B, prm, st);
-        case 3: return launch_pass1_t<NORM, VEC, 4, true>(x, y, n, A, B, prm, st);
-        default: return launch_pass1_t<NORM, VEC, 4, false>(x, y, n, A, B, prm, st);
+        default: return launch_pass1_t<NORM, VEC, 2, false>(x, y, n, A, B, prm, st);
     }
 }
 

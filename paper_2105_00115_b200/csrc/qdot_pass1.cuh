@@ -31,8 +31,9 @@
 constexpr int P1_T = 256;                    // threads per CTA
 constexpr int P1_W = 16;                     // keys with per-thread private slots
 constexpr int P1_CW = 128;                   // keys with per-CTA 32-bit limb tables
-// private window keys keep e in [-1022, 1021] (fl(x*y) normal and finite)
-constexpr int P1_SAFE_LO = KOFF - 1022;
+// private window keys keep e in [-971, 1021]: fl(x*y) normal and finite and
+// 2^(52-e) representable
+constexpr int P1_SAFE_LO = KOFF - 971;
 constexpr int P1_SAFE_HI = KOFF + 1021 - P1_W + 1;
 
 struct __align__(16) P1Shared {
@@ -121,44 +122,44 @@ __device__ __noinline__ void p1_special(P1Shared& S, int64_t* __restrict__ A, in
     p1_cold(S, A, B, key, kd, mant_bits(bx), mant_bits(by), -(int32_t)((bx ^ by) >> 63));
 }
 
-// one element
+// one element.  Private-window elements (both factors normal, key in the
+// window, which lies inside e in [-971, 1021]): fl(x*y) * 2^(52-e) is an exact
+// integer in [2^52, 2^54] -> one conversion gives the signed DOUBLE units.
 template <bool FULL>
 __device__ __forceinline__ void p1_elem(P1Shared& S, ulonglong2* __restrict__ my, int kbias,
                                         int64_t* __restrict__ A, int64_t* __restrict__ B, double xv, double yv,
                                         uint32_t* zc, uint32_t* nf) {
-    uint64_t bx = dbits(xv), by = dbits(yv);
-    uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
-    uint32_t esum = fx + fy;                                            // e + 2046
-    bool normal = (fx - 1u < 0x7FEu) & (fy - 1u < 0x7FEu) & (esum - 1024u < 2044u);   // e in [-1022, 1021]
-    if (normal) {
-        // DOUBLE: fl(x*y) in units of 2^(e-52)  (emulate.py:133)
-        uint64_t pb = dbits(__dmul_rn(xv, yv));
-        uint64_t pm = (pb & 0xFFFFFFFFFFFFFull) | (1ull << 52);
-        int sh = (int)((uint32_t)(pb >> 52) & 0x7FFu) + 1023 - (int)esum;          // 0..2
-        int64_t kd = (int64_t)(pm << sh);
-        int64_t sg = (int64_t)((int32_t)(uint32_t)(pb >> 32) >> 31);             // 0 / -1
-        kd = (kd ^ sg) - sg;
-        const int rel = (int)esum + kbias;                                        // key - base
-        if ((unsigned)rel < (unsigned)P1_W) {
-            ulonglong2* slot = my + rel * P1_T;
-            ulonglong2 v = *slot;
-            v.x += (unsigned long long)kd;
-            if (FULL) {
-                int32_t ks, kh;
-                exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
-                               bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
-                int32_t s32 = (int32_t)sg;
-                ks = (ks ^ s32) - s32;
-                kh = (kh ^ s32) - s32;
-                v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
-            } else {
-                v.y += 1ull;
-            }
-            *slot = v;
+    const uint32_t hx = (uint32_t)(dbits(xv) >> 32), hy = (uint32_t)(dbits(yv) >> 32);
+    const uint32_t fx = (hx >> 20) & 0x7FFu, fy = (hy >> 20) & 0x7FFu;
+    const uint32_t esum = fx + fy;                                      // e + 2046
+    const int rel = (int)esum + kbias;                                  // key - base
+    const bool hot = (max(fx - 1u, fy - 1u) < 0x7FEu) & ((unsigned)rel < (unsigned)P1_W);
+    if (hot) {
+        // DOUBLE (emulate.py:133): fl(x*y) in units of 2^(e-52)
+        const double scale = __hiloint2double((int)((3121u - esum) << 20), 0);   // 2^(52-e)
+        const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv, yv), scale));
+        ulonglong2* slot = my + rel * P1_T;
+        ulonglong2 v = *slot;
+        v.x += (unsigned long long)kd;
+        if (FULL) {
+            const uint64_t bx = dbits(xv), by = dbits(yv);
+            int32_t ks, kh;
+            exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
+                           bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
+            const int32_t s32 = (int32_t)(hx ^ hy) >> 31;
+            ks = (ks ^ s32) - s32;
+            kh = (kh ^ s32) - s32;
+            v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
         } else {
-            p1_cold(S, A, B, (int)esum - 2046 + KOFF, kd, (bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull,
-                    (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)sg);
+            v.y = (unsigned long long)((uint32_t)v.y + 1u);   // count < 2^32 between flushes
         }
+        *slot = v;
+    } else if ((max(fx - 1u, fy - 1u) < 0x7FEu) & (esum - 1024u < 2044u)) {  // normal, e in [-1022, 1021]
+        const uint64_t bx = dbits(xv), by = dbits(yv);
+        const int e = (int)esum - 2046;
+        const int64_t kd = double_units(dbits(__dmul_rn(xv, yv)), e);
+        p1_cold(S, A, B, e + KOFF, kd, (bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull,
+                (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)(hx ^ hy) >> 31);
     } else {
         p1_special(S, A, B, xv, yv, zc, nf);
     }
@@ -189,7 +190,7 @@ __device__ __forceinline__ void p1_flush(P1Shared& S, int64_t* __restrict__ A, i
                 long long s = (w1 - h) >> 21;
                 cs += c; hs += h; ss += s;
             } else {
-                cs += (long long)v.y;
+                cs += (long long)(uint32_t)v.y;
             }
         }
         for (int o = 16; o; o >>= 1) {
@@ -267,10 +268,14 @@ __device__ __forceinline__ void p1_tile(P1Shared& S, ulonglong2* __restrict__ my
                                         int64_t* __restrict__ A, int64_t* __restrict__ B,
                                         const double (&xv)[2 * V], const double (&yv)[2 * V], int64_t e0,
                                         int64_t n, bool fulltile, int tid, uint32_t* zc, uint32_t* nf) {
+    if (fulltile) {
 #pragma unroll
-    for (int j = 0; j < 2 * V; ++j) {
-        if (fulltile || (e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1) < n))
-            p1_elem<FULL>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+        for (int j = 0; j < 2 * V; ++j) p1_elem<FULL>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 2 * V; ++j)
+            if (e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1) < n)
+                p1_elem<FULL>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
     }
 }
 
