@@ -47,7 +47,7 @@ EPS = 1e-8
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU")
@@ -86,12 +86,14 @@ def profile_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons; only samples received inside the
+    timed window [mark_start, mark_stop] are kept."""
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def start(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -99,7 +101,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.idx), "-lms", "100"],
+                                          "-i", str(self.idx), "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -108,11 +110,18 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_stop(self):
+        self.t1 = time.perf_counter()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -120,7 +129,9 @@ class ClockSampler:
             self.proc.kill()
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for t, ln in self.lines:
+            if self.t0 is not None and not (self.t0 <= t <= (self.t1 or t) + 0.06):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -201,6 +212,7 @@ def main():
     import paper_2105_00115_b200 as Q
     from paper_2105_00115_b200 import _lib
     from paper_2105_00115_b200.device import config_struct, thread_state
+    from paper_2105_00115_b200.dist import reduce_regions
     lib = _lib.load()
 
     n = args.n
@@ -231,11 +243,11 @@ def main():
         if i is not None:
             ev_p1[i][1].record(stream)
         if world > 1:
-            torch.distributed.all_reduce(ra)
+            reduce_regions(ra)                       # NCCL SUM of region A (histogram)
         _lib.check(lib.qdot_b200_score(ws, n_total, ctypes.byref(c), s), lib)
         _lib.check(lib.qdot_b200_pass2(xp, yp, n, norm, ws, s), lib)
         if world > 1:
-            torch.distributed.all_reduce(rb)
+            reduce_regions(rb)                       # NCCL SUM of region B (exact partials)
         _lib.check(lib.qdot_b200_finalize(ws, s), lib)
 
     for _ in range(max(3, args.warmup)):
@@ -253,11 +265,13 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
+    clk.mark_start()
     t0.record(stream)
     for i in range(args.steps):
         step(i)
     t1.record(stream)
     torch.cuda.synchronize()
+    clk.mark_stop()
     if world > 1:
         torch.distributed.barrier()
     clocks = clk.stop()
@@ -276,20 +290,36 @@ def main():
 
     # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region
     e2e = None
-    if world == 1 and args.e2e_steps > 0:
+    if args.e2e_steps > 0:
+        # public API from pinned host memory: qdot() at N=1, dist.qdot_sharded()
+        # (each rank copies its own shard) at N>1; max over ranks
+        from paper_2105_00115_b200.dist import qdot_sharded
         xpin = torch.from_numpy(xh).pin_memory()
         ypin = xpin if args.norm else torch.from_numpy(yh).pin_memory()
-        rep = Q.qdot(xpin, ypin, cfg)  # warm
+
+        def api():
+            if world == 1:
+                return Q.qdot(xpin, ypin, cfg)
+            return qdot_sharded(xpin, ypin, cfg, n_total=n_total)
+
+        rep = api()  # warm
         assert rep.value == value_check
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         te = time.perf_counter()
         for _ in range(args.e2e_steps):
-            rep = Q.qdot(xpin, ypin, cfg)
+            rep = api()
         torch.cuda.synchronize()
         dte = (time.perf_counter() - te) / args.e2e_steps
+        if world > 1:
+            tt = torch.tensor([dte], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            dte = float(tt[0])
         h2d = n * 8 * (1 if args.norm else 2)
-        e2e = {"value": n / dte, "unit": "elements/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": 256 + 56 * 64, "ms_per_step": dte * 1e3}
+        e2e = {"value": n_total / dte, "unit": "elements/s", "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": (256 + 56 * 64) * world, "ms_per_step": dte * 1e3,
+               "api": "qdot()" if world == 1 else "dist.qdot_sharded()"}
         del xpin, ypin
 
     peak, peak_kind = measured_peak()

@@ -555,10 +555,10 @@ static int occupancy(K kern, int threads, size_t smem) {
     return occ > 0 ? occ : 1;
 }
 
-template <bool NORM, bool VEC, int V, bool PF>
+template <bool NORM, bool VEC, int V, bool PF, int L2D>
 static cudaError_t launch_pass1_t(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
                                   const P1Params& prm, cudaStream_t st) {
-    auto kern = k_pass1<NORM, VEC, V, PF>;
+    auto kern = k_pass1<NORM, VEC, V, PF, L2D>;
     const size_t smem = sizeof(P1Shared);
     static bool attr = false;
     if (!attr) {
@@ -590,9 +590,11 @@ template <bool NORM, bool VEC>
 static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
                                   const P1Params& prm, cudaStream_t st) {
     switch (p1_variant()) {
-        case 1: return launch_pass1_t<NORM, VEC, 4, false>(x, y, n, A, B, prm, st);
-        case 2: return launch_pass1_t<NORM, VEC, 2, true>(x, y, n, A, B, prm, st);
-        default: return launch_pass1_t<NORM, VEC, 2, false>(x, y, n, A, B, prm, st);
+        case 1: return launch_pass1_t<NORM, VEC, 4, false, 0>(x, y, n, A, B, prm, st);   // no L2 prefetch
+        case 2: return launch_pass1_t<NORM, VEC, 2, false, 3>(x, y, n, A, B, prm, st);
+        case 3: return launch_pass1_t<NORM, VEC, 4, false, 2>(x, y, n, A, B, prm, st);
+        case 4: return launch_pass1_t<NORM, VEC, 2, true, 0>(x, y, n, A, B, prm, st);    // register double buffer
+        default: return launch_pass1_t<NORM, VEC, 4, false, 3>(x, y, n, A, B, prm, st);  // tuned on B200
     }
 }
 

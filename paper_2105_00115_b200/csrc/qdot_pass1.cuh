@@ -279,9 +279,20 @@ __device__ __forceinline__ void p1_tile(P1Shared& S, ulonglong2* __restrict__ my
     }
 }
 
+// bulk prefetch of one tile of x (and y) into L2 (TMA, no registers / smem):
+// the demand loads of that tile later hit L2
+template <bool NORM>
+__device__ __forceinline__ void p1_prefetch_l2(const double* x, const double* y, int64_t n, int64_t tile, int TILE) {
+    const int64_t e0 = tile * TILE;
+    if (e0 + TILE > n) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(x + e0), "r"(TILE * 8) : "memory");
+    if (!NORM) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(y + e0), "r"(TILE * 8) : "memory");
+}
+
 // persistent loop over tiles.  PF: register double buffering (the loads of
 // the CTA's next tile are in flight while the current one is processed).
-template <bool NORM, bool VEC, bool FULL, int V, bool PF>
+// L2D > 0: one thread per CTA bulk-prefetches the tile L2D+1 iterations ahead into L2.
+template <bool NORM, bool VEC, bool FULL, int V, bool PF, int L2D>
 __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ x, const double* __restrict__ y,
                                         int64_t n, int64_t* __restrict__ A, int64_t* __restrict__ B, int tid,
                                         uint32_t* zc, uint32_t* nf) {
@@ -294,9 +305,13 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
     ulonglong2* __restrict__ my = S.priv + tid;
     int since = 0;
     if (!PF) {
+        if (L2D > 0 && tid == 0) {   // warm the first prefetch window
+            for (int d = 1; d <= L2D; ++d) p1_prefetch_l2<NORM>(x, y, n, blockIdx.x + d * stride, TILE);
+        }
         for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
             double xv[EPT], yv[EPT];
             bool f;
+            if (L2D > 0 && tid == 0) p1_prefetch_l2<NORM>(x, y, n, t + (L2D + 1) * stride, TILE);
             p1_load<NORM, VEC, V>(x, y, n, t, tid, xv, yv, f);
             p1_tile<FULL, V>(S, my, kbias, A, B, xv, yv, t * TILE, n, f, tid, zc, nf);
             if (++since == FLUSH) { p1_flush<FULL>(S, A, B, tid); since = 0; }
@@ -322,7 +337,7 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
     p1_flush<FULL>(S, A, B, tid);
 }
 
-template <bool NORM, bool VEC, int V, bool PF>
+template <bool NORM, bool VEC, int V, bool PF, int L2D>
 __global__ void __launch_bounds__(P1_T, 3)
 k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         int64_t* __restrict__ A, int64_t* __restrict__ B, P1Params prm) {
@@ -445,8 +460,8 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     // ---- main streaming loop (persistent grid over tiles)
     uint32_t zc = 0, nf = 0;
     const bool fullmode = S.full != 0;
-    if (fullmode) p1_main<NORM, VEC, true, V, PF>(S, x, y, n, A, B, tid, &zc, &nf);
-    else p1_main<NORM, VEC, false, V, PF>(S, x, y, n, A, B, tid, &zc, &nf);
+    if (fullmode) p1_main<NORM, VEC, true, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
+    else p1_main<NORM, VEC, false, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
 
     // ---- publish CTA partials (the cold table was pushed by the last flush)
     for (int r = tid; r < P1_W; r += P1_T) {

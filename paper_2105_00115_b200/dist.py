@@ -1,0 +1,105 @@
+"""Multi-GPU qdot: one process per GPU, contiguous shards, two integer allreduces.
+
+    qdot_sharded(x_local, y_local, cfg, strategy=None, group=None) -> QdotReport
+
+Every rank holds a contiguous shard [lo, hi) of the two vectors (see
+shard_bounds).  Per call and rank (all stream-ordered, one host sync at the end):
+
+    begin -> pass1(local shard)                      histogram + exact partials
+          -> allreduce(region A, SUM)  [NCCL]        ~67 KB: histogram, zero count,
+                                                      non-finite count, hot flags
+          -> score (identical inputs on every rank -> identical bins everywhere)
+          -> pass2(local shard)                      only if scoring asked for it
+          -> allreduce(region B, SUM)  [NCCL]        ~300 KB: exact per-key partials
+          -> finalize -> fetch
+
+Both regions hold integers (counts and 32-bit limbs in int64 words), so the
+sums are exact and the result is bit-identical for any number of ranks and
+any reduction order -- the same bins, precisions and value as one device
+running over the concatenated vectors.  The reference has no distributed
+path; this is the B200 build's sharding of the same result.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Tuple
+
+from . import _lib
+from .binning import ExactBinning, Strategy
+from .device import as_device_vector, config_struct, require_cuda, stream_handle, thread_state
+from .kernel import QdotReport, _raise_status, report_from_result
+from .scoring import ToleranceConfig
+
+
+def shard_bounds(n: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous, balanced shard [lo, hi) of n elements for `rank` of `world`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def reduce_regions(region_a, region_b=None, group=None) -> None:
+    """In-place SUM allreduce of the workspace regions (int64 tensors).
+
+    Backend-agnostic (NCCL for CUDA tensors, gloo for CPU tensors in tests);
+    exactness relies only on integer addition."""
+    import torch.distributed as dist
+    dist.all_reduce(region_a, op=dist.ReduceOp.SUM, group=group)
+    if region_b is not None:
+        dist.all_reduce(region_b, op=dist.ReduceOp.SUM, group=group)
+
+
+class _ShardedIndexer:
+    """Bin.indices of a sharded report would need an all-gather; refuse loudly."""
+
+    def materialize(self, params):
+        raise RuntimeError("Bin.indices is not materialised for sharded qdot reports "
+                           "(each rank holds only its shard)")
+
+
+def qdot_sharded(x_local, y_local, cfg: ToleranceConfig, strategy: Strategy = None, group=None,
+                 n_total: Optional[int] = None, reference=None) -> QdotReport:
+    """qdot over vectors sharded across the ranks of `group` (collective call).
+
+    x_local, y_local: this rank's contiguous shard (CUDA tensors or
+    array-likes).  Returns the same report on every rank, equal to
+    qdot(concat(x), concat(y), cfg, strategy) on one device.
+    """
+    import torch
+    import torch.distributed as dist
+    require_cuda()
+    if strategy is None:
+        strategy = ExactBinning()
+    is_norm = x_local is y_local
+    device = torch.device("cuda", torch.cuda.current_device())
+    xd, _ = as_device_vector(x_local, device)
+    yd = xd if is_norm else as_device_vector(y_local, device)[0]
+    if xd.shape[0] != yd.shape[0]:
+        raise ValueError(f"length mismatch: {xd.shape[0]} vs {yd.shape[0]}")
+    n = int(xd.shape[0])
+    if n_total is None:
+        t = torch.tensor([n], dtype=torch.int64, device=device)
+        dist.all_reduce(t, group=group)
+        n_total = int(t.item())
+    lib = _lib.load()
+    st = thread_state(device)
+    c = config_struct(cfg, strategy)
+    s = stream_handle(device)
+    ws = st.ws_ptr
+    xp = xd.data_ptr()
+    yp = xp if is_norm else yd.data_ptr()
+    _lib.check(lib.qdot_b200_begin(ws, s), lib)
+    _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(is_norm), ctypes.byref(c), n_total, ws, s), lib)
+    reduce_regions(st.region_a(), None, group)
+    _lib.check(lib.qdot_b200_score(ws, n_total, ctypes.byref(c), s), lib)
+    _lib.check(lib.qdot_b200_pass2(xp, yp, n, int(is_norm), ws, s), lib)
+    dist.all_reduce(st.region_b(), op=dist.ReduceOp.SUM, group=group)
+    _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+    _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
+    _raise_status(st.result)
+    phase = {"select": 0, "compute": 0, "reference": 0}
+    return report_from_result(st.result, st.bins, cfg, strategy, is_norm, reference, phase, _ShardedIndexer())

@@ -254,3 +254,27 @@ def test_c2_headline_size_properties():
         [[b.lower, b.upper, b.cardinality, b.score, b.precision] for b in r.bins]
     assert rep.value == r.value == -23532.7407708119
     assert abs(rep.value - ex) <= rep.abs_cap
+
+
+def test_qdot_sharded_single_rank_nccl():
+    """dist.qdot_sharded through a real NCCL process group (world 1 on this box;
+    the 2/4/8-rank exchange algebra is covered by tests/test_dist_cpu.py)."""
+    import socket
+    import torch.distributed as dist
+    from paper_2105_00115_b200.dist import qdot_sharded
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        x, y = O.gen_illcond(1 << 16, seed=4)
+        cfg = Q.ToleranceConfig(1e-12, Q.SplitMode.PER_BIN)
+        a = qdot_sharded(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), cfg)
+        b = Q.qdot(x, y, cfg)
+        assert a.value == b.value and a.counts == b.counts and a.abs_bound == b.abs_bound
+        assert [(u.lower, u.upper, u.cardinality) for u in a.params.bins] == \
+            [(u.lower, u.upper, u.cardinality) for u in b.params.bins]
+    finally:
+        dist.destroy_process_group()
