@@ -109,7 +109,7 @@ def config_struct(cfg, strategy) -> _lib.QdotConfig:
     code, param = strategy_code(strategy)
     c = _lib.QdotConfig()
     c.epsilon = float(cfg.epsilon)
-    c.split = 1 if cfg.split is SplitMode.PER_BIN else 0
+    c.split = 1 if cfg.split == SplitMode.PER_BIN else 0
     c.input_mu = int(cfg.input_mu)
     c.strategy = code
     c.strategy_param = param

@@ -38,6 +38,21 @@ class PrecisionLevel(enum.Enum):
         """Index used by the C ABI (qdot_precision)."""
         return LEVELS_ASC.index(self)
 
+    # Interoperate with the reference's own enum (qdot.scoring.PrecisionLevel):
+    # equal by label, same hash as an Enum member of the same name, so
+    # report.counts[<reference PrecisionLevel>] and == comparisons work.
+    def __eq__(self, other):
+        if self is other:
+            return True
+        lab = getattr(other, "label", None)
+        mb = getattr(other, "mantissa_bits", None)
+        if lab is None or mb is None:
+            return NotImplemented
+        return lab == self.label and mb == self.mantissa_bits
+
+    def __hash__(self):
+        return hash(self._name_)
+
     @classmethod
     def from_mu(cls, mu: int) -> "PrecisionLevel":
         for level in cls:
@@ -58,6 +73,15 @@ _EPS_MAX = math.ldexp(1.0, 60)
 class SplitMode(enum.Enum):
     NONE = "none"
     PER_BIN = "per-bin"
+
+    def __eq__(self, other):   # equal to the reference's SplitMode member of the same value
+        if self is other:
+            return True
+        v = getattr(other, "value", None)
+        return NotImplemented if v is None else v == self.value
+
+    def __hash__(self):
+        return hash(self._name_)
 
 
 @dataclass

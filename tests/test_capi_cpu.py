@@ -146,3 +146,29 @@ def test_strategy_parsing_and_labels():
 def test_precision_codes_match_c_enum():
     assert [p.code for p in (P.PERFORATE, P.HALF, P.SINGLE, P.DOUBLE)] == [0, 1, 2, 3]
     assert P.from_code(3) is P.DOUBLE and P.HALF.eps == 2.0**-10
+
+
+def test_enums_interoperate_with_reference_style_enums():
+    import enum
+
+    class RefLevel(enum.Enum):          # same shape as qdot.scoring.PrecisionLevel
+        PERFORATE = ("perforate", 0)
+        HALF = ("half", 10)
+        SINGLE = ("single", 23)
+        DOUBLE = ("double", 52)
+
+        def __init__(self, label, mantissa_bits):
+            self.label = label
+            self.mantissa_bits = mantissa_bits
+
+    class RefSplit(enum.Enum):
+        NONE = "none"
+        PER_BIN = "per-bin"
+
+    counts = {lvl: i for i, lvl in enumerate(P)}
+    assert counts[RefLevel.DOUBLE] == counts[P.DOUBLE]
+    assert P.HALF == RefLevel.HALF and P.HALF != RefLevel.SINGLE
+    assert Q.SplitMode.PER_BIN == RefSplit.PER_BIN
+    cfg = Q.ToleranceConfig(1e-3, split=RefSplit.PER_BIN)
+    from paper_2105_00115_b200.device import config_struct
+    assert config_struct(cfg, None).split == 1
