@@ -74,6 +74,7 @@ SIGNATURES = {
     "qdot_b200_dot_host": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), ctypes.POINTER(QdotResult),
                                 ctypes.POINTER(QdotBin), ctypes.c_int32]),
     "qdot_b200_bin_ids": (_I, [_P, _P, _I64, _I, _P, _P, _P]),
+    "qdot_b200_batched": (_I, [_P, _P, _I64, _I64, _I64, _I, ctypes.POINTER(QdotConfig), _P, _P, _P, _P]),
     "qdot_b200_ldexp_rn": (ctypes.c_double, [ctypes.c_double, _I64, ctypes.POINTER(_I)]),
 }
 

@@ -1,0 +1,328 @@
+// qdot_batched.cuh -- many independent qdots (rows of X, Y), one warp per row,
+// one HBM pass (included into namespace qd of qdot_kernels.cu).
+//
+// Per row the warp runs the whole pipeline of kernel.qdot (kernel.py:179-240)
+// for ExactBinning (and early termination at input_mu 52): exponent sums,
+// exact per-key DOUBLE / SINGLE / HALF partial sums (the "full" variants of
+// pass 1, accumulated in per-lane shared-memory slots for a 16-key window
+// and per-warp 32-bit limb tables for a 64-key window), then per-row scoring
+// (scoring.py:96-216), per-bin rounding (emulate.py:116-154) and the Neumaier
+// fold (emulate.py:157-163) -- all inside the warp, no inter-row traffic.
+//
+// Rows the fast kernel cannot finish exactly are flagged BS_GENERAL and
+// re-run by the host through the single-vector pipeline: strategies other
+// than exact binning, keys spread beyond the 64-key window, DOUBLE product
+// overflow, early termination below input_mu 52, rows longer than 2^16.
+
+constexpr int BW = 16;            // per-lane private window (keys)
+constexpr int BCW = 64;           // per-warp limb table window (keys)
+constexpr int B_WARPS = 4;        // warps (rows in flight) per CTA
+constexpr int B_MAXLEN = 1 << 16;
+
+// per-row status bits (qdot_b200_batched info[4*r + 3])
+constexpr int BS_NONFINITE = 1;
+constexpr int BS_OVERFLOW = 2;
+constexpr int BS_EPS = 4;
+constexpr int BS_GENERAL = 8;
+constexpr int BS_EARLY = 16;
+constexpr int BS_HALF_ORDER = 32;
+
+struct __align__(16) BWarp {
+    ulonglong2 priv[BW * 32];     // per-lane {D units, packed S|H|count}
+    uint32_t c[8][BCW];           // limb table: cnt, d0, d1, d2, d3 (signed), s0, s1 (signed), h (signed)
+};
+
+struct BParams {
+    double epsilon;
+    int32_t split;
+    int32_t input_mu;
+    int32_t strategy;
+    int32_t norm;
+};
+
+// flush per-lane slots into the warp's limb table (all lanes, warp-synchronous)
+__device__ __forceinline__ void b_flush(BWarp& W, int lane, int base_rel) {
+    __syncwarp();
+    for (int r = 0; r < BW; ++r) {
+        ulonglong2 v = W.priv[r * 32 + lane];
+        W.priv[r * 32 + lane] = make_ulonglong2(0ull, 0ull);
+        int64_t d = (int64_t)v.x;
+        uint64_t dlo = (uint64_t)d;
+        int64_t dhi = d >> 63;
+        long long w = (long long)v.y;
+        long long c = w & 0xFF;
+        long long w1 = (w - c) >> 8;
+        long long h = ((w1 & 0x1FFFFF) ^ 0x100000) - 0x100000;
+        long long s = (w1 - h) >> 21;
+        for (int o = 16; o; o >>= 1) {
+            uint64_t olo = __shfl_xor_sync(0xffffffffu, dlo, o);
+            int64_t ohi = __shfl_xor_sync(0xffffffffu, dhi, o);
+            uint64_t nl = dlo + olo;
+            dhi += ohi + (nl < dlo ? 1 : 0);
+            dlo = nl;
+            s += __shfl_xor_sync(0xffffffffu, s, o);
+            h += __shfl_xor_sync(0xffffffffu, h, o);
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (lane == 0 && c) {
+            const int k = base_rel + r;                      // index into the limb table
+            __int128 D = ((__int128)dhi << 64) | (__int128)dlo;
+            W.c[0][k] += (uint32_t)c;
+            W.c[1][k] += (uint32_t)((uint64_t)D & 0x3FFFu);
+            W.c[2][k] += (uint32_t)(((uint64_t)D >> 14) & 0x3FFFu);
+            W.c[3][k] += (uint32_t)(((uint64_t)D >> 28) & 0x3FFFu);
+            W.c[4][k] += (uint32_t)(int32_t)(long long)(D >> 42);
+            W.c[5][k] += (uint32_t)(s & 0x3FFF);
+            W.c[6][k] += (uint32_t)(int32_t)(s >> 14);
+            W.c[7][k] += (uint32_t)(int32_t)h;
+        }
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void b_cold_add(BWarp& W, int c, int64_t kd, int32_t ks, int32_t kh) {
+    uint64_t u = (uint64_t)kd;
+    atomicAdd(&W.c[0][c], 1u);
+    atomicAdd(&W.c[1][c], (uint32_t)(u & 0x3FFFu));
+    atomicAdd(&W.c[2][c], (uint32_t)((u >> 14) & 0x3FFFu));
+    atomicAdd(&W.c[3][c], (uint32_t)((u >> 28) & 0x3FFFu));
+    atomicAdd(&W.c[4][c], (uint32_t)(int32_t)(kd >> 42));
+    atomicAdd(&W.c[5][c], (uint32_t)ks & 0x3FFFu);
+    atomicAdd(&W.c[6][c], (uint32_t)(ks >> 14));
+    atomicAdd(&W.c[7][c], (uint32_t)kh);
+}
+
+// element outside the private window (or special): limb table or a row flag
+__device__ __noinline__ void b_other(BWarp& W, int cbase, double xv, double yv, uint32_t* zc, uint32_t* st) {
+    uint64_t bx = dbits(xv), by = dbits(yv);
+    if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) { *st |= BS_NONFINITE; return; }
+    if (xv == 0.0 || yv == 0.0) { (*zc)++; return; }
+    int e = flexp_bits(bx) + flexp_bits(by);
+    int c = e + KOFF - cbase;
+    if ((unsigned)c >= (unsigned)BCW) { *st |= BS_GENERAL; return; }
+    uint64_t pb = dbits(__dmul_rn(xv, yv));
+    if (((pb >> 52) & 0x7FF) == 0x7FF) { *st |= BS_GENERAL; return; }     // DOUBLE overflow: rare, general path
+    int64_t kd = double_units(pb, e);
+    int32_t ks, kh;
+    exact_variants(bitsd(mant_bits(bx)), bitsd(mant_bits(by)), ks, kh);
+    int32_t sg = -(int32_t)((bx ^ by) >> 63);
+    ks = (ks ^ sg) - sg;
+    kh = (kh ^ sg) - sg;
+    b_cold_add(W, c, kd, ks, kh);
+}
+
+__device__ __forceinline__ void b_elem(BWarp& W, ulonglong2* __restrict__ my, int kbias, int cbase, double xv,
+                                       double yv, uint32_t* zc, uint32_t* st) {
+    const uint32_t hx = (uint32_t)(dbits(xv) >> 32), hy = (uint32_t)(dbits(yv) >> 32);
+    const uint32_t fx = (hx >> 20) & 0x7FFu, fy = (hy >> 20) & 0x7FFu;
+    const uint32_t esum = fx + fy;
+    const int rel = (int)esum + kbias;
+    if ((max(fx - 1u, fy - 1u) < 0x7FEu) & ((unsigned)rel < (unsigned)BW)) {
+        const double scale = __hiloint2double((int)((3121u - esum) << 20), 0);   // 2^(52-e)
+        const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv, yv), scale));
+        const uint64_t bx = dbits(xv), by = dbits(yv);
+        int32_t ks, kh;
+        exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
+                       bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
+        const int32_t s32 = (int32_t)(hx ^ hy) >> 31;
+        ks = (ks ^ s32) - s32;
+        kh = (kh ^ s32) - s32;
+        ulonglong2* slot = my + rel * 32;
+        ulonglong2 v = *slot;
+        v.x += (unsigned long long)kd;
+        v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
+        *slot = v;
+    } else {
+        b_other(W, cbase, xv, yv, zc, st);
+    }
+}
+
+// exact sum of D over the row's present keys, rounded to double (early-terminated DOUBLE bin)
+__device__ double b_early_double(const int64_t* kd_lo, int kmin_c, int kmax_c, int cbase, int lane,
+                                 __int128 D0, __int128 D1, uint32_t cnt0, uint32_t cnt1, int* ovf) {
+    BigSum<104> acc;
+    int lsb = qd_double(cbase + kmin_c - KOFF);
+    acc.init(lsb, (qd_double(cbase + kmax_c - KOFF) - lsb + 160) / 32 + 2);
+    for (int j = kmin_c; j <= kmax_c; ++j) {
+        const int src = j & 31;
+        const bool hi = j >= 32;
+        uint64_t lo64 = __shfl_sync(0xffffffffu, (uint64_t)(hi ? D1 : D0), src);
+        int64_t hi64 = __shfl_sync(0xffffffffu, (int64_t)((hi ? D1 : D0) >> 64), src);
+        uint32_t c = __shfl_sync(0xffffffffu, hi ? cnt1 : cnt0, src);
+        if (c) acc.add(((__int128)hi64 << 64) | (__int128)lo64, qd_double(cbase + j - KOFF));
+    }
+    (void)kd_lo; (void)lane;
+    return acc.round(52, -1022, 1023, ovf);
+}
+
+__global__ void __launch_bounds__(B_WARPS * 32)
+k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows, int64_t len, int64_t ld,
+          BParams prm, double* __restrict__ values, int64_t* __restrict__ counts, int32_t* __restrict__ info) {
+    __shared__ BWarp warps[B_WARPS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    BWarp& W = warps[wid];
+    ulonglong2* __restrict__ my = W.priv + lane;
+    const int64_t rstride = (int64_t)gridDim.x * B_WARPS;
+    const bool vec = ((ld & 1) == 0) && ((len & 1) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(X) | (prm.norm ? 0 : reinterpret_cast<uintptr_t>(Y))) & 15u) == 0;
+    for (int64_t r = (int64_t)blockIdx.x * B_WARPS + wid; r < rows; r += rstride) {
+        const double* xr = X + r * ld;
+        const double* yr = prm.norm ? xr : Y + r * ld;
+        // bulk-prefetch the next row of this warp into L2
+        if (lane == 0 && r + rstride < rows && (len & 1) == 0 && vec) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(X + (r + rstride) * ld), "r"((int)(len * 8)) : "memory");
+            if (!prm.norm)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(Y + (r + rstride) * ld), "r"((int)(len * 8)) : "memory");
+        }
+        uint32_t st = 0, zc = 0;
+        if (prm.strategy != QDOT_STRATEGY_EXACT || len > B_MAXLEN) st |= BS_GENERAL;
+        // ---- window from the first 32 elements: mean key of normal products
+        int base;
+        {
+            int k = -1;
+            if (lane < len) {
+                uint32_t fx = (uint32_t)(dbits(xr[lane]) >> 52) & 0x7FFu, fy = (uint32_t)(dbits(yr[lane]) >> 52) & 0x7FFu;
+                if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) k = (int)(fx + fy) - 2046 + KOFF;
+            }
+            int s = k >= 0 ? k : 0, c = k >= 0 ? 1 : 0;
+            for (int o = 16; o; o >>= 1) { s += __shfl_xor_sync(0xffffffffu, s, o); c += __shfl_xor_sync(0xffffffffu, c, o); }
+            int mean = c ? (s + c / 2) / c : KOFF;
+            base = mean - BW / 2 + 1;
+            base = base < KOFF - 971 ? KOFF - 971 : (base > KOFF + 1021 - BW + 1 ? KOFF + 1021 - BW + 1 : base);
+        }
+        int cbase = base - (BCW - BW) / 2;
+        cbase = cbase < 0 ? 0 : (cbase + BCW > KEYS ? KEYS - BCW : cbase);
+        const int kbias = KOFF - 2046 - base;
+        // ---- clear this warp's state
+        for (int i = lane; i < BW * 32; i += 32) W.priv[i] = make_ulonglong2(0ull, 0ull);
+        for (int i = lane; i < 8 * BCW; i += 32) (&W.c[0][0])[i] = 0u;
+        __syncwarp();
+        // ---- stream the row (one HBM pass)
+        if (!(st & BS_GENERAL)) {
+            int since = 0;
+            if (vec) {
+                for (int64_t i = 2 * lane; i < len; i += 64) {
+                    double2 a = __ldcs(reinterpret_cast<const double2*>(xr + i));
+                    double2 b = prm.norm ? a : __ldcs(reinterpret_cast<const double2*>(yr + i));
+                    b_elem(W, my, kbias, cbase, a.x, b.x, &zc, &st);
+                    if (i + 1 < len) b_elem(W, my, kbias, cbase, a.y, b.y, &zc, &st);
+                    if (++since == 124) { b_flush(W, lane, base - cbase); since = 0; }
+                }
+            } else {
+                for (int64_t i = lane; i < len; i += 32) {
+                    double a = xr[i], b = yr[i];
+                    b_elem(W, my, kbias, cbase, a, b, &zc, &st);
+                    if (++since == 248) { b_flush(W, lane, base - cbase); since = 0; }
+                }
+            }
+            b_flush(W, lane, base - cbase);
+        }
+        // row-wide status and zero count
+        for (int o = 16; o; o >>= 1) {
+            st |= __shfl_xor_sync(0xffffffffu, st, o);
+            zc += __shfl_xor_sync(0xffffffffu, zc, o);
+        }
+        double value = 0.0;
+        long long cnt_p[4] = {0, 0, 0, 0};
+        int nbins = 0, emin = 0, emax = 0;
+        if (!(st & (BS_GENERAL | BS_NONFINITE))) {
+            // ---- per-key totals: lane owns table entries j = lane and lane + 32
+            uint32_t cnt[2];
+            __int128 D[2];
+            long long S[2], H[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = lane + 32 * h;
+                cnt[h] = W.c[0][j];
+                D[h] = (__int128)W.c[1][j] + ((__int128)W.c[2][j] << 14) + ((__int128)W.c[3][j] << 28) +
+                       ((__int128)(int32_t)W.c[4][j] << 42);
+                S[h] = (long long)W.c[5][j] + ((long long)(int32_t)W.c[6][j] << 14);
+                H[h] = (long long)(int32_t)W.c[7][j];
+            }
+            const unsigned pres0 = __ballot_sync(0xffffffffu, cnt[0] != 0);
+            const unsigned pres1 = __ballot_sync(0xffffffffu, cnt[1] != 0);
+            nbins = __popc(pres0) + __popc(pres1);
+            if (nbins) {
+                const int jmin = pres0 ? __ffs(pres0) - 1 : 32 + __ffs(pres1) - 1;
+                const int jmax = pres1 ? 63 - __clz(pres1) : 31 - __clz(pres0);
+                emin = cbase + jmin - KOFF;
+                emax = cbase + jmax - KOFF;
+                bool okf = true;
+                const long long fle = flexp_bits(dbits(prm.epsilon));
+                const int mu_hat = prm.input_mu == 52 ? 23 : (prm.input_mu == 23 ? 10 : 0);
+                const bool early = (long long)(emax - emin) <= (-fle - mu_hat);           // scoring.py:126-136
+                long long nnz = 0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) nnz += cnt[h];
+                for (int o = 16; o; o >>= 1) nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+                if (early) {
+                    st |= BS_EARLY;
+                    if (prm.input_mu != 52) st |= BS_GENERAL;
+                    nbins = 1;
+                    // single bin (e_min-1, e_max], M = nnz, eps_eff = eps (one bin)
+                    long long mm = nnz - 1;
+                    long long sc = (mm ? 64 - __clzll(mm) : 0) + 0 - fle + 1;
+                    int pr = precision_of(sc, prm.input_mu);
+                    int ovf = 0;
+                    if (pr == QDOT_DOUBLE) value = b_early_double(nullptr, jmin, jmax, cbase, lane, D[0], D[1], cnt[0], cnt[1], &ovf);
+                    else if (pr != QDOT_PERFORATE) st |= BS_GENERAL;
+                    if (lane == 0) cnt_p[pr] += nnz;
+                } else {
+                    double eps_eff = prm.split == 1 ? __ddiv_rn(prm.epsilon, (double)nbins) : prm.epsilon;
+                    long long fl = floor_log2_d(eps_eff, &okf);
+                    if (!okf) st |= BS_EPS;
+                    double val[2] = {0.0, 0.0};
+                    int pr[2] = {0, 0};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (!cnt[h]) continue;
+                        const int e = cbase + lane + 32 * h - KOFF;
+                        unsigned long long mm = cnt[h] - 1;
+                        long long sc = (mm ? 64 - __clzll((long long)mm) : 0) + e - emax - fl + 1;   // bin_score
+                        pr[h] = precision_of(sc, prm.input_mu);
+                        int ovf = 0;
+                        if (pr[h] == QDOT_DOUBLE) {
+                            val[h] = round_i128(D[h], qd_double(e), 52, -1022, 1023, &ovf);
+                        } else if (pr[h] == QDOT_SINGLE) {
+                            val[h] = ldexp_rn(round_i128((__int128)S[h], -23, 52, -1022, 1023, &ovf), e, &ovf);
+                        } else if (pr[h] == QDOT_HALF) {
+                            val[h] = ldexp_rn(round_i128((__int128)H[h], -10, 23, -126, 127, &ovf), e, &ovf);
+                            if ((double)cnt[h] * 4.0 > 16384.0) st |= BS_HALF_ORDER;
+                        }
+                        if (ovf) st |= BS_OVERFLOW;
+                        cnt_p[pr[h]] += cnt[h];
+                    }
+                    // Neumaier fold over bins in ascending key order (emulate.py:157-163)
+                    double s = 0.0, c = 0.0;
+                    unsigned rem0 = pres0, rem1 = pres1;
+                    while (rem0 | rem1) {
+                        int j;
+                        if (rem0) { j = __ffs(rem0) - 1; rem0 &= rem0 - 1; }
+                        else { j = 32 + __ffs(rem1) - 1; rem1 &= rem1 - 1; }
+                        const double v = __shfl_sync(0xffffffffu, j < 32 ? val[0] : val[1], j & 31);
+                        const double t = __dadd_rn(s, v);
+                        if (fabs(s) >= fabs(v)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), v));
+                        else c = __dadd_rn(c, __dadd_rn(__dsub_rn(v, t), s));
+                        s = t;
+                    }
+                    value = (s - s == 0.0) ? __dadd_rn(s, c) : s;
+                }
+                for (int p = 0; p < 4; ++p)
+                    for (int o = 16; o; o >>= 1) cnt_p[p] += __shfl_xor_sync(0xffffffffu, cnt_p[p], o);
+                for (int o = 16; o; o >>= 1) st |= __shfl_xor_sync(0xffffffffu, st, o);
+            }
+        }
+        if (lane == 0) {
+            values[r] = value;
+            counts[4 * r + 0] = cnt_p[0] + zc;
+            counts[4 * r + 1] = cnt_p[1];
+            counts[4 * r + 2] = cnt_p[2];
+            counts[4 * r + 3] = cnt_p[3];
+            info[4 * r + 0] = nbins;
+            info[4 * r + 1] = emin;
+            info[4 * r + 2] = emax;
+            info[4 * r + 3] = (int32_t)st;
+        }
+        __syncwarp();
+    }
+}

@@ -255,6 +255,17 @@ int qdot_b200_bin_ids(const double* x, const double* y, int64_t n, int norm, con
     return QDOT_OK;
 }
 
+int qdot_b200_batched(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, int norm,
+                      const qdot_config* cfg, double* values, int64_t* counts, int32_t* info, void* stream) {
+    int v = validate(cfg);
+    if (v) return v;
+    if (rows < 0 || len < 0 || ld < len || (rows > 0 && (!X || (!norm && !Y) || !values || !counts || !info)))
+        return QDOT_ERR_ARG;
+    QD_CHECK(launch_batched(X, Y, rows, len, ld, norm != 0, *cfg, values, counts, info,
+                            static_cast<cudaStream_t>(stream)), "batched");
+    return QDOT_OK;
+}
+
 double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow) {
     int o = 0;
     double r = ldexp_rn(acc, u, &o);

@@ -36,6 +36,8 @@ constexpr int SC_PER = (KEYS + SC_T - 1) / SC_T;   // 5 keys per thread
 
 struct ScShared {
     unsigned long long off[KEYS + 1];   // exclusive prefix of counts over keys
+    long long bup[KEYS];                // per-bin upper bound (staged for the LUT pass)
+    signed char bprec[KEYS];            // per-bin precision
     int first[KEYS];
     int last[KEYS];
     int bin_of[KEYS];
@@ -294,6 +296,8 @@ k_score(const int64_t* __restrict__ A, int32_t* __restrict__ lut_bin, uint32_t* 
         ob.precision = precision_of(score, cfg.input_mu);
         ob.first_key = f; ob.last_key = l; ob.flags = 0; ob.value = 0.0;
         bins[b] = ob;
+        S.bup[b] = upper;
+        S.bprec[b] = (signed char)ob.precision;
     }
     __syncthreads();
     __threadfence_block();
@@ -304,8 +308,8 @@ k_score(const int64_t* __restrict__ A, int32_t* __restrict__ lut_bin, uint32_t* 
         lut_bin[k] = b;
         uint32_t d = 0;
         if (b >= 0) {
-            int pr = bins[b].precision;
-            long long delta = bins[b].upper - (long long)(k - KOFF);
+            int pr = S.bprec[b];
+            long long delta = S.bup[b] - (long long)(k - KOFF);
             if ((pr == QDOT_HALF || pr == QDOT_SINGLE) && (delta > 0 || A[A_HOT + k] > 0) &&
                 S.s_status == QDOT_OK) {
                 d = P2_NEED | (pr == QDOT_HALF ? P2_HALF : 0u) |
@@ -427,84 +431,127 @@ __device__ __forceinline__ __int128 key_double(const int64_t* __restrict__ B, in
     return v;
 }
 
+// round an exact signed integer v * 2^lsb to a binary format (see round_scaled)
+__device__ __forceinline__ double round_i128(__int128 v, int lsb, int mu, int emin, int emax, int* ovf) {
+    if (v == 0) return 0.0;
+    const bool neg = v < 0;
+    unsigned __int128 a = neg ? (unsigned __int128)(-v) : (unsigned __int128)v;
+    const uint64_t hi = (uint64_t)(a >> 64);
+    if (!hi) return round_scaled((uint64_t)a, lsb, false, neg, mu, emin, emax, ovf);
+    const int sh = 64 - clz64(hi);                 // bits above the low 64
+    const uint64_t top = (uint64_t)(a >> sh);
+    const bool sticky = (a & (((unsigned __int128)1 << sh) - 1)) != 0;
+    return round_scaled(top, lsb + sh, sticky, neg, mu, emin, emax, ovf);
+}
+
+constexpr int FN_CHUNK = 1024;
+
 __global__ void __launch_bounds__(FN_T, 1)
 k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const uint32_t* __restrict__ lut_p2,
            const ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
+    __shared__ double s_val[FN_CHUNK];
+    __shared__ long long s_card[FN_CHUNK];
+    __shared__ signed char s_prec[FN_CHUNK];
     __shared__ int s_ovf, s_half;
+    __shared__ double s_s, s_c;
+    __shared__ long long s_cnt[4];
     const int tid = threadIdx.x;
     const ScoreMeta m = *meta;
-    if (tid == 0) { s_ovf = 0; s_half = 0; }
+    if (tid == 0) { s_ovf = 0; s_half = 0; s_s = 0.0; s_c = 0.0; s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0; }
     __syncthreads();
     const int nb = m.status == QDOT_OK ? m.n_bins : 0;
-    for (int b = tid; b < nb; b += FN_T) {
-        qdot_bin bn = bins[b];
-        const int f = bn.first_key, l = bn.last_key;
-        const long long u = bn.upper;
-        double val = 0.0;
-        int flags = 0;
-        if (bn.precision == QDOT_DOUBLE) {
-            long long ip = 0, in = 0;
-            for (int k = f; k <= l; ++k) { ip += B[B_INFP + k]; in += B[B_INFN + k]; }
-            if (ip && in) val = __longlong_as_double(0x7FF8000000000000ll);
-            else if (ip) val = INFINITY;
-            else if (in) val = -INFINITY;
-            else {
-                BigSum<104> acc;
-                int lsb = qd_double(f - KOFF);
-                acc.init(lsb, (qd_double(l - KOFF) - lsb + 160) / 32 + 2);
-                for (int k = f; k <= l; ++k)
-                    if (A[A_CNT + k]) acc.add(key_double(B, k), qd_double(k - KOFF));
+    for (int base = 0; base < nb; base += FN_CHUNK) {
+        const int cn = nb - base < FN_CHUNK ? nb - base : FN_CHUNK;
+        for (int i = tid; i < cn; i += FN_T) {
+            const int b = base + i;
+            const qdot_bin bn = bins[b];
+            const int f = bn.first_key, l = bn.last_key;
+            const long long u = bn.upper;
+            double val = 0.0;
+            int flags = 0;
+            if (bn.precision == QDOT_DOUBLE) {                                  // emulate.py:132-133
+                long long ip = 0, in = 0;
+                for (int k = f; k <= l; ++k) { ip += B[B_INFP + k]; in += B[B_INFN + k]; }
                 int ovf = 0;
-                val = acc.round(52, -1022, 1023, &ovf);
+                if (ip && in) val = __longlong_as_double(0x7FF8000000000000ll);
+                else if (ip) val = INFINITY;
+                else if (in) val = -INFINITY;
+                else if (f == l) val = round_i128(key_double(B, f), qd_double(f - KOFF), 52, -1022, 1023, &ovf);
+                else {
+                    BigSum<104> acc;
+                    int lsb = qd_double(f - KOFF);
+                    acc.init(lsb, (qd_double(l - KOFF) - lsb + 160) / 32 + 2);
+                    for (int k = f; k <= l; ++k)
+                        if (A[A_CNT + k]) acc.add(key_double(B, k), qd_double(k - KOFF));
+                    val = acc.round(52, -1022, 1023, &ovf);
+                }
+            } else if (bn.precision != QDOT_PERFORATE) {                         // emulate.py:135-154
+                const bool half = bn.precision == QDOT_HALF;
+                const int mu = half ? 10 : 23;
+                const int qmin_fmt = half ? -24 : -149;
+                auto qs_of = [&](int k) {
+                    long long d = u - (long long)(k - KOFF);
+                    int dd = d > P2_DELTA_MAX ? P2_DELTA_MAX : (int)d;
+                    return -dd - mu > qmin_fmt ? -dd - mu : qmin_fmt;
+                };
+                auto keyval = [&](int k) -> long long {
+                    return (lut_p2[k] & P2_NEED) ? B[B_P2 + k] : (half ? B[B_H0 + k] : B[B_S0 + k]);
+                };
+                const int lsb = qs_of(f);
+                double mass = 0.0;   // bound on sum |p| (scaled domain) for the fp32-exactness check
+                double a;
+                int ovf = 0;
+                if (f == l) {
+                    a = half ? round_i128((__int128)keyval(f), lsb, 23, -126, 127, &ovf)
+                             : round_i128((__int128)keyval(f), lsb, 52, -1022, 1023, &ovf);
+                    long long d = u - (long long)(f - KOFF);
+                    mass = (double)A[A_CNT + f] * ldexp(4.0, (int)(d > 2000 ? -2000 : -d));
+                } else {
+                    BigSum<16> acc;
+                    acc.init(lsb, (qs_of(l) - lsb + 128) / 32 + 2);
+                    for (int k = f; k <= l; ++k) {
+                        long long c = A[A_CNT + k];
+                        if (!c) continue;
+                        long long d = u - (long long)(k - KOFF);
+                        acc.add((__int128)keyval(k), qs_of(k));
+                        mass += (double)c * ldexp(4.0, (int)(d > 2000 ? -2000 : -d));
+                    }
+                    a = half ? acc.round(23, -126, 127, &ovf) : acc.round(52, -1022, 1023, &ovf);
+                }
+                val = ldexp_rn(a, u, &ovf);                                       // emulate.py:154
+                if (ovf) atomicOr(&s_ovf, 1);
+                if (half && mass > ldexp(1.0, 24 + lsb)) { flags |= 1; atomicOr(&s_half, 1); }
             }
-        } else if (bn.precision != QDOT_PERFORATE) {
-            const bool half = bn.precision == QDOT_HALF;
-            const int mu = half ? 10 : 23;
-            const int qmin_fmt = half ? -24 : -149;
-            auto qs_of = [&](int k) {
-                long long d = u - (long long)(k - KOFF);
-                int dd = d > P2_DELTA_MAX ? P2_DELTA_MAX : (int)d;
-                return -dd - mu > qmin_fmt ? -dd - mu : qmin_fmt;
-            };
-            BigSum<16> acc;
-            int lsb = qs_of(f);
-            acc.init(lsb, (qs_of(l) - lsb + 128) / 32 + 2);
-            double mass = 0.0;   // bound on sum |p| (scaled domain) for the fp32-exactness check
-            for (int k = f; k <= l; ++k) {
-                long long c = A[A_CNT + k];
-                if (!c) continue;
-                long long d = u - (long long)(k - KOFF);
-                long long v = (lut_p2[k] & P2_NEED) ? B[B_P2 + k] : (half ? B[B_H0 + k] : B[B_S0 + k]);
-                acc.add((__int128)v, qs_of(k));
-                mass += (double)c * ldexp(4.0, (int)(d > 2000 ? -2000 : -d));
-            }
-            int ovf = 0;
-            double a = half ? acc.round(23, -126, 127, &ovf) : acc.round(52, -1022, 1023, &ovf);
-            val = ldexp_rn(a, u, &ovf);                                       // emulate.py:154
-            if (ovf) atomicOr(&s_ovf, 1);
-            if (half && mass > ldexp(1.0, 24 + lsb)) { flags |= 1; atomicOr(&s_half, 1); }
+            bins[b].value = val;
+            bins[b].flags = flags;
+            s_val[i] = val;
+            s_card[i] = bn.cardinality;
+            s_prec[i] = (signed char)bn.precision;
         }
-        bins[b].value = val;
-        bins[b].flags = flags;
+        __syncthreads();
+        if (tid == 0) {
+            // qdot_accumulate: Neumaier over bins in ascending-upper order (emulate.py:55-72)
+            double sum = s_s, c = s_c;
+            for (int i = 0; i < cn; ++i) {
+                const double v = s_val[i];
+                const double t = __dadd_rn(sum, v);
+                if (fabs(sum) >= fabs(v)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(sum, t), v));
+                else c = __dadd_rn(c, __dadd_rn(__dsub_rn(v, t), sum));
+                sum = t;
+                s_cnt[s_prec[i]] += s_card[i];
+            }
+            s_s = sum;
+            s_c = c;
+        }
+        __syncthreads();
     }
-    __syncthreads();
     if (tid == 0) {
         qdot_result r;
         memset(&r, 0, sizeof(r));
-        // qdot_accumulate: Neumaier over bins in ascending-upper order (emulate.py:55-72)
-        double s = 0.0, c = 0.0;
-        long long cnts[4] = {0, 0, 0, 0};
-        for (int b = 0; b < nb; ++b) {
-            double v = bins[b].value;
-            double t = __dadd_rn(s, v);
-            if (fabs(s) >= fabs(v)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(s, t), v));
-            else c = __dadd_rn(c, __dadd_rn(__dsub_rn(v, t), s));
-            s = t;
-            cnts[bins[b].precision] += bins[b].cardinality;
-        }
-        r.value = (s - s == 0.0) ? __dadd_rn(s, c) : s;
-        cnts[QDOT_PERFORATE] += m.zero;                                         // kernel.py:175
-        for (int i = 0; i < 4; ++i) r.counts[i] = cnts[i];
+        const double sum = s_s;
+        r.value = (sum - sum == 0.0) ? __dadd_rn(sum, s_c) : sum;
+        for (int i = 0; i < 4; ++i) r.counts[i] = s_cnt[i];
+        r.counts[QDOT_PERFORATE] += m.zero;                                    // kernel.py:175
         r.eps_eff = m.eps_eff;
         r.n = m.n_total;
         r.nnz = m.nnz;
@@ -519,6 +566,8 @@ k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const u
         *res = r;
     }
 }
+
+#include "qdot_batched.cuh"
 
 // =============================================================================
 // bin ids (lazy Bin.indices)
@@ -654,6 +703,24 @@ cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm,
 cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
                             qdot_result* res, qdot_bin* bins, cudaStream_t st) {
     k_finalize<<<1, FN_T, 0, st>>>(A, B, lut_p2, meta, res, bins);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batched(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, bool norm,
+                           const qdot_config& cfg, double* values, int64_t* counts, int32_t* info, cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    BParams prm;
+    prm.epsilon = cfg.epsilon;
+    prm.split = cfg.split;
+    prm.input_mu = cfg.input_mu;
+    prm.strategy = cfg.strategy;
+    prm.norm = norm ? 1 : 0;
+    static int occ = 0;
+    if (!occ) occ = occupancy(k_batched, B_WARPS * 32, 0);
+    int64_t grid = (rows + B_WARPS - 1) / B_WARPS;
+    int64_t cap = (int64_t)sm_count_cached() * occ;
+    if (grid > cap) grid = cap;
+    k_batched<<<(unsigned)grid, B_WARPS * 32, 0, st>>>(X, norm ? X : Y, rows, len, ld, prm, values, counts, info);
     return cudaGetLastError();
 }
 

@@ -20,6 +20,8 @@ cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm,
                          const ScoreMeta* meta, int64_t* B, cudaStream_t st);
 cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
                             qdot_result* res, qdot_bin* bins, cudaStream_t st);
+cudaError_t launch_batched(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, bool norm,
+                           const qdot_config& cfg, double* values, int64_t* counts, int32_t* info, cudaStream_t st);
 cudaError_t launch_bin_ids(const double* x, const double* y, int64_t n, bool norm, const int32_t* lut_bin,
                            int32_t* out, cudaStream_t st);
 

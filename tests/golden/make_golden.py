@@ -193,6 +193,25 @@ def main():
     add("C3_2e20", x, y, 1e-12, "none", "exact", store=False)
     add("C3_2e20_perbin", x, y, 1e-12, "per-bin", "exact", store=False)
 
+    # --- C4 batched rows (BASELINE configs[3]): X, Y = default_rng(0) standard normal (65536, 4096)
+    rng = np.random.default_rng(0)
+    X = rng.standard_normal((65536, 4096))
+    Y = rng.standard_normal((65536, 4096))
+    for r in [0, 1, 2, 65535]:
+        add(f"C4_row{r}", X[r].copy(), Y[r].copy(), 1e-6, "none", "exact", key=f"C4_row{r}")
+    del X, Y
+    # --- batched parity matrix: 48 rows of mixed families, length 1024
+    rng = np.random.default_rng(21)
+    for r in range(48):
+        fam = "AB"[r % 2]
+        t = [6, 14, 30, 60][r % 4]
+        x, y = gen_family(fam, t, 1024, 5000 + r)
+        if r % 5 == 0:
+            x[rng.integers(0, 1024, 40)] = 0.0
+        eps = [1e-2, 1e-5, 1e-8, 1e-12][r % 4]
+        sp = "per-bin" if r % 3 == 0 else "none"
+        add(f"batch_{r}", x, y, eps, sp, "exact", key=f"batch_{r}")
+
     np.savez_compressed(os.path.join(HERE, "golden_inputs.npz"), **inputs)
     with open(os.path.join(HERE, "golden_cases.json"), "w") as f:
         json.dump({"reference": "qdot 0.1.0 (/root/reference/pkg/src)",
