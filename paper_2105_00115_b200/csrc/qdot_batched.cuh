@@ -18,6 +18,7 @@ constexpr int BW = 16;            // per-lane private window (keys)
 constexpr int BCW = 64;           // per-warp limb table window (keys)
 constexpr int B_WARPS = 4;        // warps (rows in flight) per CTA
 constexpr int B_MAXLEN = 1 << 16;
+constexpr int B_PFD = 4;          // L2 prefetch distance (warp iterations of 128 elements)
 
 // per-row status bits (qdot_b200_batched info[4*r + 3])
 constexpr int BS_NONFINITE = 1;
@@ -168,12 +169,6 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
     for (int64_t r = (int64_t)blockIdx.x * B_WARPS + wid; r < rows; r += rstride) {
         const double* xr = X + r * ld;
         const double* yr = prm.norm ? xr : Y + r * ld;
-        // bulk-prefetch the next row of this warp into L2
-        if (lane == 0 && r + rstride < rows && (len & 1) == 0 && vec) {
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(X + (r + rstride) * ld), "r"((int)(len * 8)) : "memory");
-            if (!prm.norm)
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(Y + (r + rstride) * ld), "r"((int)(len * 8)) : "memory");
-        }
         uint32_t st = 0, zc = 0;
         if (prm.strategy != QDOT_STRATEGY_EXACT || len > B_MAXLEN) st |= BS_GENERAL;
         // ---- window from the first 32 elements: mean key of normal products
@@ -199,21 +194,37 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
         __syncwarp();
         // ---- stream the row (one HBM pass)
         if (!(st & BS_GENERAL)) {
+            // warp-uniform trip count (b_flush is warp-collective); 128 elements per
+            // warp iteration, TMA bulk L2 prefetch of the chunk B_PFD iterations ahead
             int since = 0;
-            if (vec) {
-                for (int64_t i = 2 * lane; i < len; i += 64) {
-                    double2 a = __ldcs(reinterpret_cast<const double2*>(xr + i));
-                    double2 b = prm.norm ? a : __ldcs(reinterpret_cast<const double2*>(yr + i));
-                    b_elem(W, my, kbias, cbase, a.x, b.x, &zc, &st);
-                    if (i + 1 < len) b_elem(W, my, kbias, cbase, a.y, b.y, &zc, &st);
-                    if (++since == 124) { b_flush(W, lane, base - cbase); since = 0; }
+            for (int64_t i0 = 0; i0 < len; i0 += 128) {
+                if (vec && lane == 0 && i0 + (B_PFD + 1) * 128 <= len) {
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(xr + i0 + B_PFD * 128), "r"(1024) : "memory");
+                    if (!prm.norm)
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(yr + i0 + B_PFD * 128), "r"(1024) : "memory");
                 }
-            } else {
-                for (int64_t i = lane; i < len; i += 32) {
-                    double a = xr[i], b = yr[i];
-                    b_elem(W, my, kbias, cbase, a, b, &zc, &st);
-                    if (++since == 248) { b_flush(W, lane, base - cbase); since = 0; }
+                double xa[4], ya[4];
+                bool ok[4];
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int64_t i = i0 + v * 64 + 2 * lane;
+                    ok[2 * v] = i < len;
+                    ok[2 * v + 1] = i + 1 < len;
+                    if (vec && ok[2 * v + 1]) {
+                        double2 a = __ldcs(reinterpret_cast<const double2*>(xr + i));
+                        double2 b = prm.norm ? a : __ldcs(reinterpret_cast<const double2*>(yr + i));
+                        xa[2 * v] = a.x; xa[2 * v + 1] = a.y; ya[2 * v] = b.x; ya[2 * v + 1] = b.y;
+                    } else {
+                        xa[2 * v] = ok[2 * v] ? xr[i] : 0.0;
+                        ya[2 * v] = ok[2 * v] ? yr[i] : 0.0;
+                        xa[2 * v + 1] = ok[2 * v + 1] ? xr[i + 1] : 0.0;
+                        ya[2 * v + 1] = ok[2 * v + 1] ? yr[i + 1] : 0.0;
+                    }
                 }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (ok[j]) b_elem(W, my, kbias, cbase, xa[j], ya[j], &zc, &st);
+                if (++since == 62) { b_flush(W, lane, base - cbase); since = 0; }   // <= 248 elements per lane
             }
             b_flush(W, lane, base - cbase);
         }
