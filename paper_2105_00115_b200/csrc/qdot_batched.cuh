@@ -81,6 +81,9 @@ __device__ __forceinline__ void b_flush(BWarp& W, int lane, int base_rel) {
     __syncwarp();
 }
 
+// key - cbase from key - base: base = KOFF - 2046 - kbias
+__device__ __forceinline__ int kbias_to_c(int kbias, int cbase) { return (KOFF - 2046 - kbias) - cbase; }
+
 __device__ __forceinline__ void b_cold_add(BWarp& W, int c, int64_t kd, int32_t ks, int32_t kh) {
     uint64_t u = (uint64_t)kd;
     atomicAdd(&W.c[0][c], 1u);
@@ -93,8 +96,8 @@ __device__ __forceinline__ void b_cold_add(BWarp& W, int c, int64_t kd, int32_t 
     atomicAdd(&W.c[7][c], (uint32_t)kh);
 }
 
-// element outside the private window (or special): limb table or a row flag
-__device__ __noinline__ void b_other(BWarp& W, int cbase, double xv, double yv, uint32_t* zc, uint32_t* st) {
+// zero / subnormal / non-finite / extreme elements: limb table or a row flag
+__device__ __noinline__ void b_special(BWarp& W, int cbase, double xv, double yv, uint32_t* zc, uint32_t* st) {
     uint64_t bx = dbits(xv), by = dbits(yv);
     if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) { *st |= BS_NONFINITE; return; }
     if (xv == 0.0 || yv == 0.0) { (*zc)++; return; }
@@ -118,7 +121,10 @@ __device__ __forceinline__ void b_elem(BWarp& W, ulonglong2* __restrict__ my, in
     const uint32_t fx = (hx >> 20) & 0x7FFu, fy = (hy >> 20) & 0x7FFu;
     const uint32_t esum = fx + fy;
     const int rel = (int)esum + kbias;
-    if ((max(fx - 1u, fy - 1u) < 0x7FEu) & ((unsigned)rel < (unsigned)BW)) {
+    const int crel = rel + (kbias_to_c(kbias, cbase));
+    const bool normal = max(fx - 1u, fy - 1u) < 0x7FEu;
+    if (normal & ((unsigned)rel < (unsigned)BW | ((unsigned)crel < (unsigned)BCW & (esum - 1075u < 1993u)))) {
+        // e in the private window, or in the limb-table window with 2^(52-e) representable
         const double scale = __hiloint2double((int)((3121u - esum) << 20), 0);   // 2^(52-e)
         const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv, yv), scale));
         const uint64_t bx = dbits(xv), by = dbits(yv);
@@ -128,13 +134,17 @@ __device__ __forceinline__ void b_elem(BWarp& W, ulonglong2* __restrict__ my, in
         const int32_t s32 = (int32_t)(hx ^ hy) >> 31;
         ks = (ks ^ s32) - s32;
         kh = (kh ^ s32) - s32;
-        ulonglong2* slot = my + rel * 32;
-        ulonglong2 v = *slot;
-        v.x += (unsigned long long)kd;
-        v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
-        *slot = v;
+        if ((unsigned)rel < (unsigned)BW) {
+            ulonglong2* slot = my + rel * 32;
+            ulonglong2 v = *slot;
+            v.x += (unsigned long long)kd;
+            v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
+            *slot = v;
+        } else {
+            b_cold_add(W, crel, kd, ks, kh);
+        }
     } else {
-        b_other(W, cbase, xv, yv, zc, st);
+        b_special(W, cbase, xv, yv, zc, st);
     }
 }
 
@@ -171,18 +181,38 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
         const double* yr = prm.norm ? xr : Y + r * ld;
         uint32_t st = 0, zc = 0;
         if (prm.strategy != QDOT_STRATEGY_EXACT || len > B_MAXLEN) st |= BS_GENERAL;
-        // ---- window from the first 32 elements: mean key of normal products
+        // ---- window from the first 64 elements: among windows [k-W+3, k+2] anchored
+        // at sampled keys k, the one covering most samples (ties: lower base)
         int base;
         {
-            int k = -1;
-            if (lane < len) {
-                uint32_t fx = (uint32_t)(dbits(xr[lane]) >> 52) & 0x7FFu, fy = (uint32_t)(dbits(yr[lane]) >> 52) & 0x7FFu;
-                if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) k = (int)(fx + fy) - 2046 + KOFF;
+            int k2[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = lane + 32 * h;
+                k2[h] = -10000;
+                if (i < len) {
+                    uint32_t fx = (uint32_t)(dbits(xr[i]) >> 52) & 0x7FFu, fy = (uint32_t)(dbits(yr[i]) >> 52) & 0x7FFu;
+                    if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) k2[h] = (int)(fx + fy) - 2046 + KOFF;
+                }
             }
-            int s = k >= 0 ? k : 0, c = k >= 0 ? 1 : 0;
-            for (int o = 16; o; o >>= 1) { s += __shfl_xor_sync(0xffffffffu, s, o); c += __shfl_xor_sync(0xffffffffu, c, o); }
-            int mean = c ? (s + c / 2) / c : KOFF;
-            base = mean - BW / 2 + 1;
+            int best = -1, bbase = KOFF - BW / 2;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cand = k2[h] - BW + 3;       // candidate window [cand, cand + BW)
+                int cov = 0;
+                for (int src = 0; src < 32; ++src) {
+                    const int a = __shfl_sync(0xffffffffu, k2[0], src), b = __shfl_sync(0xffffffffu, k2[1], src);
+                    cov += ((unsigned)(a - cand) < (unsigned)BW) + ((unsigned)(b - cand) < (unsigned)BW);
+                }
+                if (k2[h] >= 0 && (cov > best || (cov == best && cand < bbase))) { best = cov; bbase = cand; }
+            }
+            // warp argmax of (coverage, -base)
+            long long key = best < 0 ? -1ll : (((long long)best << 32) | (uint32_t)(0x7FFFFFFF - bbase));
+            for (int o = 16; o; o >>= 1) {
+                long long t = __shfl_xor_sync(0xffffffffu, key, o);
+                key = t > key ? t : key;
+            }
+            base = key < 0 ? KOFF - BW / 2 : (int)(0x7FFFFFFF - (uint32_t)(key & 0xFFFFFFFF));
             base = base < KOFF - 971 ? KOFF - 971 : (base > KOFF + 1021 - BW + 1 ? KOFF + 1021 - BW + 1 : base);
         }
         int cbase = base - (BCW - BW) / 2;
