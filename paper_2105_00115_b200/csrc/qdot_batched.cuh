@@ -18,7 +18,8 @@ constexpr int BW = 16;            // per-lane private window (keys)
 constexpr int BCW = 64;           // per-warp limb table window (keys)
 constexpr int B_WARPS = 4;        // warps (rows in flight) per CTA
 constexpr int B_MAXLEN = 1 << 16;
-constexpr int B_PFD = 4;          // L2 prefetch distance (warp iterations of 128 elements)
+constexpr int B_CHUNK = 512;      // L2 prefetch granule (elements; 4 warp iterations)
+constexpr int B_PFC = 2;          // prefetch distance in chunks
 
 // per-row status bits (qdot_b200_batched info[4*r + 3])
 constexpr int BS_NONFINITE = 1;
@@ -41,42 +42,54 @@ struct BParams {
     int32_t norm;
 };
 
-// flush per-lane slots into the warp's limb table (all lanes, warp-synchronous)
+// flush per-lane slots into the warp's limb table (all lanes, warp-synchronous).
+// Transposed: lane L sums key (L & 15) over lanes 16*(L >> 4) .. +15 (staggered
+// so each 8-lane LDS.128 phase touches 8 distinct bank groups), one xor-16
+// shuffle merges the halves, lanes 0..15 update the table.
 __device__ __forceinline__ void b_flush(BWarp& W, int lane, int base_rel) {
     __syncwarp();
-    for (int r = 0; r < BW; ++r) {
-        ulonglong2 v = W.priv[r * 32 + lane];
-        W.priv[r * 32 + lane] = make_ulonglong2(0ull, 0ull);
-        int64_t d = (int64_t)v.x;
-        uint64_t dlo = (uint64_t)d;
-        int64_t dhi = d >> 63;
-        long long w = (long long)v.y;
-        long long c = w & 0xFF;
-        long long w1 = (w - c) >> 8;
-        long long h = ((w1 & 0x1FFFFF) ^ 0x100000) - 0x100000;
-        long long s = (w1 - h) >> 21;
-        for (int o = 16; o; o >>= 1) {
-            uint64_t olo = __shfl_xor_sync(0xffffffffu, dlo, o);
-            int64_t ohi = __shfl_xor_sync(0xffffffffu, dhi, o);
-            uint64_t nl = dlo + olo;
-            dhi += ohi + (nl < dlo ? 1 : 0);
-            dlo = nl;
-            s += __shfl_xor_sync(0xffffffffu, s, o);
-            h += __shfl_xor_sync(0xffffffffu, h, o);
-            c += __shfl_xor_sync(0xffffffffu, c, o);
-        }
-        if (lane == 0 && c) {
-            const int k = base_rel + r;                      // index into the limb table
-            __int128 D = ((__int128)dhi << 64) | (__int128)dlo;
-            W.c[0][k] += (uint32_t)c;
-            W.c[1][k] += (uint32_t)((uint64_t)D & 0x3FFFu);
-            W.c[2][k] += (uint32_t)(((uint64_t)D >> 14) & 0x3FFFu);
-            W.c[3][k] += (uint32_t)(((uint64_t)D >> 28) & 0x3FFFu);
-            W.c[4][k] += (uint32_t)(int32_t)(long long)(D >> 42);
-            W.c[5][k] += (uint32_t)(s & 0x3FFF);
-            W.c[6][k] += (uint32_t)(int32_t)(s >> 14);
-            W.c[7][k] += (uint32_t)(int32_t)h;
-        }
+    const int k = lane & 15, half = lane >> 4;
+    uint64_t dlo = 0;
+    int64_t dhi = 0;
+    long long s = 0, h = 0, c = 0;
+#pragma unroll 4
+    for (int j = 0; j < 16; ++j) {
+        const int idx = k * 32 + half * 16 + ((j + k) & 15);
+        const ulonglong2 v = W.priv[idx];
+        W.priv[idx] = make_ulonglong2(0ull, 0ull);
+        const int64_t d = (int64_t)v.x;
+        const uint64_t nl = dlo + (uint64_t)d;
+        dhi += (d >> 63) + (nl < dlo ? 1 : 0);
+        dlo = nl;
+        const long long w = (long long)v.y;
+        const long long cc = w & 0xFF;
+        const long long w1 = (w - cc) >> 8;
+        const long long hh = ((w1 & 0x1FFFFF) ^ 0x100000) - 0x100000;
+        c += cc;
+        h += hh;
+        s += (w1 - hh) >> 21;
+    }
+    {
+        const uint64_t olo = __shfl_xor_sync(0xffffffffu, dlo, 16);
+        const int64_t ohi = __shfl_xor_sync(0xffffffffu, dhi, 16);
+        const uint64_t nl = dlo + olo;
+        dhi += ohi + (nl < dlo ? 1 : 0);
+        dlo = nl;
+        s += __shfl_xor_sync(0xffffffffu, s, 16);
+        h += __shfl_xor_sync(0xffffffffu, h, 16);
+        c += __shfl_xor_sync(0xffffffffu, c, 16);
+    }
+    if (half == 0 && c) {
+        const int t = base_rel + k;                          // index into the limb table
+        const __int128 D = ((__int128)dhi << 64) | (__int128)dlo;
+        W.c[0][t] += (uint32_t)c;
+        W.c[1][t] += (uint32_t)((uint64_t)D & 0x3FFFu);
+        W.c[2][t] += (uint32_t)(((uint64_t)D >> 14) & 0x3FFFu);
+        W.c[3][t] += (uint32_t)(((uint64_t)D >> 28) & 0x3FFFu);
+        W.c[4][t] += (uint32_t)(int32_t)(long long)(D >> 42);
+        W.c[5][t] += (uint32_t)(s & 0x3FFF);
+        W.c[6][t] += (uint32_t)(int32_t)(s >> 14);
+        W.c[7][t] += (uint32_t)(int32_t)h;
     }
     __syncwarp();
 }
@@ -96,8 +109,9 @@ __device__ __forceinline__ void b_cold_add(BWarp& W, int c, int64_t kd, int32_t 
     atomicAdd(&W.c[7][c], (uint32_t)kh);
 }
 
-// zero / subnormal / non-finite / extreme elements: limb table or a row flag
-__device__ __noinline__ void b_special(BWarp& W, int cbase, double xv, double yv, uint32_t* zc, uint32_t* st) {
+// everything outside the private window: limb-table keys, zero / subnormal /
+// non-finite / extreme elements (limb table or a row flag)
+__device__ __noinline__ void b_cold(BWarp& W, int cbase, double xv, double yv, uint32_t* zc, uint32_t* st) {
     uint64_t bx = dbits(xv), by = dbits(yv);
     if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) { *st |= BS_NONFINITE; return; }
     if (xv == 0.0 || yv == 0.0) { (*zc)++; return; }
@@ -115,16 +129,16 @@ __device__ __noinline__ void b_special(BWarp& W, int cbase, double xv, double yv
     b_cold_add(W, c, kd, ks, kh);
 }
 
+// one element: private-window keys (both factors normal; the window lies in
+// e in [-971, 1021], so 2^(52-e) is representable and fl(x*y) normal) inline,
+// everything else through b_cold
 __device__ __forceinline__ void b_elem(BWarp& W, ulonglong2* __restrict__ my, int kbias, int cbase, double xv,
                                        double yv, uint32_t* zc, uint32_t* st) {
     const uint32_t hx = (uint32_t)(dbits(xv) >> 32), hy = (uint32_t)(dbits(yv) >> 32);
     const uint32_t fx = (hx >> 20) & 0x7FFu, fy = (hy >> 20) & 0x7FFu;
     const uint32_t esum = fx + fy;
     const int rel = (int)esum + kbias;
-    const int crel = rel + (kbias_to_c(kbias, cbase));
-    const bool normal = max(fx - 1u, fy - 1u) < 0x7FEu;
-    if (normal & ((unsigned)rel < (unsigned)BW | ((unsigned)crel < (unsigned)BCW & (esum - 1075u < 1993u)))) {
-        // e in the private window, or in the limb-table window with 2^(52-e) representable
+    if (((unsigned)rel < (unsigned)BW) & (max(fx - 1u, fy - 1u) < 0x7FEu)) {
         const double scale = __hiloint2double((int)((3121u - esum) << 20), 0);   // 2^(52-e)
         const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv, yv), scale));
         const uint64_t bx = dbits(xv), by = dbits(yv);
@@ -134,17 +148,13 @@ __device__ __forceinline__ void b_elem(BWarp& W, ulonglong2* __restrict__ my, in
         const int32_t s32 = (int32_t)(hx ^ hy) >> 31;
         ks = (ks ^ s32) - s32;
         kh = (kh ^ s32) - s32;
-        if ((unsigned)rel < (unsigned)BW) {
-            ulonglong2* slot = my + rel * 32;
-            ulonglong2 v = *slot;
-            v.x += (unsigned long long)kd;
-            v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
-            *slot = v;
-        } else {
-            b_cold_add(W, crel, kd, ks, kh);
-        }
+        ulonglong2* slot = my + rel * 32;
+        ulonglong2 v = *slot;
+        v.x += (unsigned long long)kd;
+        v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
+        *slot = v;
     } else {
-        b_special(W, cbase, xv, yv, zc, st);
+        b_cold(W, cbase, xv, yv, zc, st);
     }
 }
 
@@ -166,6 +176,57 @@ __device__ double b_early_double(const int64_t* kd_lo, int kmin_c, int kmax_c, i
     return acc.round(52, -1022, 1023, ovf);
 }
 
+// bulk L2 prefetch of chunk `c` (B_CHUNK elements) of the warp's stream, which
+// continues into its next row; lane 0 only
+__device__ __forceinline__ void b_prefetch(const double* xr, const double* yr, const double* xn, const double* yn,
+                                           int64_t len, int64_t c, bool norm) {
+    int64_t e0 = c * B_CHUNK;
+    const double *px = xr, *py = yr;
+    if (e0 >= len) {
+        if (!xn) return;
+        e0 -= len;
+        px = xn;
+        py = yn;
+    }
+    if (e0 + B_CHUNK > len) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(px + e0), "r"(B_CHUNK * 8) : "memory");
+    if (!norm) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(py + e0), "r"(B_CHUNK * 8) : "memory");
+}
+
+// warp iteration: 128 elements, lane holds {2l, 2l+1, 64+2l, 65+2l}
+template <bool NORM>
+__device__ __forceinline__ void b_load_full(const double* __restrict__ xr, const double* __restrict__ yr, int64_t i0,
+                                            int lane, double (&xa)[4], double (&ya)[4]) {
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+        const int64_t i = i0 + v * 64 + 2 * lane;
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(xr + i));
+        xa[2 * v] = a.x;
+        xa[2 * v + 1] = a.y;
+        if (NORM) {
+            ya[2 * v] = a.x;
+            ya[2 * v + 1] = a.y;
+        } else {
+            const double2 b = __ldcs(reinterpret_cast<const double2*>(yr + i));
+            ya[2 * v] = b.x;
+            ya[2 * v + 1] = b.y;
+        }
+    }
+}
+
+template <bool NORM>
+__device__ __forceinline__ void b_load_tail(const double* __restrict__ xr, const double* __restrict__ yr, int64_t i0,
+                                            int64_t len, int lane, double (&xa)[4], double (&ya)[4], bool (&ok)[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t i = i0 + (j >> 1) * 64 + 2 * lane + (j & 1);
+        ok[j] = i < len;
+        xa[j] = ok[j] ? xr[i] : 0.0;
+        ya[j] = ok[j] ? (NORM ? xa[j] : yr[i]) : 0.0;
+    }
+}
+
+template <bool NORM, bool VEC>
 __global__ void __launch_bounds__(B_WARPS * 32)
 k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows, int64_t len, int64_t ld,
           BParams prm, double* __restrict__ values, int64_t* __restrict__ counts, int32_t* __restrict__ info) {
@@ -174,87 +235,100 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
     BWarp& W = warps[wid];
     ulonglong2* __restrict__ my = W.priv + lane;
     const int64_t rstride = (int64_t)gridDim.x * B_WARPS;
-    const bool vec = ((ld & 1) == 0) && ((len & 1) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(X) | (prm.norm ? 0 : reinterpret_cast<uintptr_t>(Y))) & 15u) == 0;
+    const int64_t nfull = VEC ? len / 128 : 0;            // full warp iterations per row
+    for (int i = lane; i < BW * 32; i += 32) W.priv[i] = make_ulonglong2(0ull, 0ull);   // flushes keep it zero
     for (int64_t r = (int64_t)blockIdx.x * B_WARPS + wid; r < rows; r += rstride) {
         const double* xr = X + r * ld;
-        const double* yr = prm.norm ? xr : Y + r * ld;
+        const double* yr = NORM ? xr : Y + r * ld;
+        const bool has_next = r + rstride < rows;
+        const double* xn = has_next ? X + (r + rstride) * ld : nullptr;
+        const double* yn = has_next ? (NORM ? xn : Y + (r + rstride) * ld) : nullptr;
         uint32_t st = 0, zc = 0;
         if (prm.strategy != QDOT_STRATEGY_EXACT || len > B_MAXLEN) st |= BS_GENERAL;
-        // ---- window from the first 64 elements: among windows [k-W+3, k+2] anchored
-        // at sampled keys k, the one covering most samples (ties: lower base)
+        // ---- first warp iteration: doubles as the sample that places the windows
+        double xa[4], ya[4], xb[4], yb[4];
+        bool ok0[4] = {true, true, true, true};
+        if (nfull > 0) b_load_full<NORM>(xr, yr, 0, lane, xa, ya);
+        else b_load_tail<NORM>(xr, yr, 0, len, lane, xa, ya, ok0);
+        if (VEC && lane == 0 && r == (int64_t)blockIdx.x * B_WARPS + wid)   // first row: warm its stream
+            for (int64_t c = 1; c < B_PFC; ++c) b_prefetch(xr, yr, xn, yn, len, c, NORM);
         int base;
         {
-            int k2[2];
+            int k4[4];
+            int kmx = -1;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int i = lane + 32 * h;
-                k2[h] = -10000;
-                if (i < len) {
-                    uint32_t fx = (uint32_t)(dbits(xr[i]) >> 52) & 0x7FFu, fy = (uint32_t)(dbits(yr[i]) >> 52) & 0x7FFu;
-                    if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) k2[h] = (int)(fx + fy) - 2046 + KOFF;
-                }
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t fx = (uint32_t)(dbits(xa[j]) >> 52) & 0x7FFu, fy = (uint32_t)(dbits(ya[j]) >> 52) & 0x7FFu;
+                k4[j] = (ok0[j] && fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) ? (int)(fx + fy) - 2046 + KOFF : -10000;
+                kmx = max(kmx, k4[j]);
             }
-            int best = -1, bbase = KOFF - BW / 2;
+            for (int o = 16; o; o >>= 1) kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+            // window [kmax - W + 3, kmax + 2] when it holds >= 3/4 of the sample
+            int cand = kmx - BW + 3, cov = 0, nv = 0;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int cand = k2[h] - BW + 3;       // candidate window [cand, cand + BW)
-                int cov = 0;
-                for (int src = 0; src < 32; ++src) {
-                    const int a = __shfl_sync(0xffffffffu, k2[0], src), b = __shfl_sync(0xffffffffu, k2[1], src);
-                    cov += ((unsigned)(a - cand) < (unsigned)BW) + ((unsigned)(b - cand) < (unsigned)BW);
+            for (int j = 0; j < 4; ++j) {
+                cov += __popc(__ballot_sync(0xffffffffu, (unsigned)(k4[j] - cand) < (unsigned)BW));
+                nv += __popc(__ballot_sync(0xffffffffu, k4[j] >= 0));
+            }
+            if (nv == 0) {
+                base = KOFF - BW / 2;
+            } else if (4 * cov >= 3 * nv) {
+                base = cand;
+            } else {
+                // among windows anchored at sampled keys, the one covering most samples
+                long long bestkey = -1;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int cd = k4[h] - BW + 3;
+                    int cv = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        for (int src = 0; src < 32; ++src) {
+                            const int a = __shfl_sync(0xffffffffu, k4[j], src);
+                            cv += (unsigned)(a - cd) < (unsigned)BW;
+                        }
+                    const long long key = k4[h] < 0 ? -1ll : (((long long)cv << 32) | (uint32_t)(0x7FFFFFFF - cd));
+                    bestkey = key > bestkey ? key : bestkey;
                 }
-                if (k2[h] >= 0 && (cov > best || (cov == best && cand < bbase))) { best = cov; bbase = cand; }
+                for (int o = 16; o; o >>= 1) {
+                    const long long t = __shfl_xor_sync(0xffffffffu, bestkey, o);
+                    bestkey = t > bestkey ? t : bestkey;
+                }
+                base = (int)(0x7FFFFFFF - (uint32_t)(bestkey & 0xFFFFFFFF));
             }
-            // warp argmax of (coverage, -base)
-            long long key = best < 0 ? -1ll : (((long long)best << 32) | (uint32_t)(0x7FFFFFFF - bbase));
-            for (int o = 16; o; o >>= 1) {
-                long long t = __shfl_xor_sync(0xffffffffu, key, o);
-                key = t > key ? t : key;
-            }
-            base = key < 0 ? KOFF - BW / 2 : (int)(0x7FFFFFFF - (uint32_t)(key & 0xFFFFFFFF));
             base = base < KOFF - 971 ? KOFF - 971 : (base > KOFF + 1021 - BW + 1 ? KOFF + 1021 - BW + 1 : base);
         }
         int cbase = base - (BCW - BW) / 2;
         cbase = cbase < 0 ? 0 : (cbase + BCW > KEYS ? KEYS - BCW : cbase);
         const int kbias = KOFF - 2046 - base;
-        // ---- clear this warp's state
-        for (int i = lane; i < BW * 32; i += 32) W.priv[i] = make_ulonglong2(0ull, 0ull);
+        // ---- clear this warp's limb table (the private slots are zero after every flush)
         for (int i = lane; i < 8 * BCW; i += 32) (&W.c[0][0])[i] = 0u;
         __syncwarp();
-        // ---- stream the row (one HBM pass)
+        // ---- stream the row (one HBM pass); trip counts are warp-uniform (b_flush is collective)
         if (!(st & BS_GENERAL)) {
-            // warp-uniform trip count (b_flush is warp-collective); 128 elements per
-            // warp iteration, TMA bulk L2 prefetch of the chunk B_PFD iterations ahead
             int since = 0;
-            for (int64_t i0 = 0; i0 < len; i0 += 128) {
-                if (vec && lane == 0 && i0 + (B_PFD + 1) * 128 <= len) {
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(xr + i0 + B_PFD * 128), "r"(1024) : "memory");
-                    if (!prm.norm)
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(yr + i0 + B_PFD * 128), "r"(1024) : "memory");
-                }
-                double xa[4], ya[4];
-                bool ok[4];
+            auto step = [&](int64_t it, double (&cx)[4], double (&cy)[4], double (&nx)[4], double (&ny)[4]) {
+                if (it + 1 < nfull) b_load_full<NORM>(xr, yr, (it + 1) * 128, lane, nx, ny);
+                if (lane == 0 && (it & (B_CHUNK / 128 - 1)) == 0)
+                    b_prefetch(xr, yr, xn, yn, len, it / (B_CHUNK / 128) + B_PFC, NORM);
 #pragma unroll
-                for (int v = 0; v < 2; ++v) {
-                    const int64_t i = i0 + v * 64 + 2 * lane;
-                    ok[2 * v] = i < len;
-                    ok[2 * v + 1] = i + 1 < len;
-                    if (vec && ok[2 * v + 1]) {
-                        double2 a = __ldcs(reinterpret_cast<const double2*>(xr + i));
-                        double2 b = prm.norm ? a : __ldcs(reinterpret_cast<const double2*>(yr + i));
-                        xa[2 * v] = a.x; xa[2 * v + 1] = a.y; ya[2 * v] = b.x; ya[2 * v + 1] = b.y;
-                    } else {
-                        xa[2 * v] = ok[2 * v] ? xr[i] : 0.0;
-                        ya[2 * v] = ok[2 * v] ? yr[i] : 0.0;
-                        xa[2 * v + 1] = ok[2 * v + 1] ? xr[i + 1] : 0.0;
-                        ya[2 * v + 1] = ok[2 * v + 1] ? yr[i + 1] : 0.0;
-                    }
-                }
+                for (int j = 0; j < 4; ++j) b_elem(W, my, kbias, cbase, cx[j], cy[j], &zc, &st);
+                if (++since == 62) { b_flush(W, lane, base - cbase); since = 0; }   // <= 248 elements per lane
+            };
+            int64_t it = 0;
+            for (; it + 2 <= nfull; it += 2) {
+                step(it, xa, ya, xb, yb);
+                step(it + 1, xb, yb, xa, ya);
+            }
+            if (it < nfull) { step(it, xa, ya, xb, yb); ++it; }
+            // ragged tail (and every iteration when the rows are not 16-byte aligned)
+            for (int64_t i0 = it * 128; i0 < len; i0 += 128) {
+                bool ok[4];
+                b_load_tail<NORM>(xr, yr, i0, len, lane, xa, ya, ok);
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                     if (ok[j]) b_elem(W, my, kbias, cbase, xa[j], ya[j], &zc, &st);
-                if (++since == 62) { b_flush(W, lane, base - cbase); since = 0; }   // <= 248 elements per lane
+                if (++since == 62) { b_flush(W, lane, base - cbase); since = 0; }
             }
             b_flush(W, lane, base - cbase);
         }

@@ -706,6 +706,11 @@ cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* 
     return cudaGetLastError();
 }
 
+template <bool NORM, bool VEC>
+static cudaError_t launch_batched_t(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld,
+                                    const BParams& prm, double* values, int64_t* counts, int32_t* info,
+                                    cudaStream_t st);
+
 cudaError_t launch_batched(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, bool norm,
                            const qdot_config& cfg, double* values, int64_t* counts, int32_t* info, cudaStream_t st) {
     if (rows <= 0) return cudaSuccess;
@@ -715,12 +720,25 @@ cudaError_t launch_batched(const double* X, const double* Y, int64_t rows, int64
     prm.input_mu = cfg.input_mu;
     prm.strategy = cfg.strategy;
     prm.norm = norm ? 1 : 0;
+    const bool vec = ((ld & 1) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(X) | (norm ? 0 : reinterpret_cast<uintptr_t>(Y))) & 15u) == 0;
+    if (norm) return vec ? launch_batched_t<true, true>(X, X, rows, len, ld, prm, values, counts, info, st)
+                         : launch_batched_t<true, false>(X, X, rows, len, ld, prm, values, counts, info, st);
+    return vec ? launch_batched_t<false, true>(X, Y, rows, len, ld, prm, values, counts, info, st)
+               : launch_batched_t<false, false>(X, Y, rows, len, ld, prm, values, counts, info, st);
+}
+
+template <bool NORM, bool VEC>
+static cudaError_t launch_batched_t(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld,
+                                    const BParams& prm, double* values, int64_t* counts, int32_t* info,
+                                    cudaStream_t st) {
+    auto kern = k_batched<NORM, VEC>;
     static int occ = 0;
-    if (!occ) occ = occupancy(k_batched, B_WARPS * 32, 0);
+    if (!occ) occ = occupancy(kern, B_WARPS * 32, 0);
     int64_t grid = (rows + B_WARPS - 1) / B_WARPS;
     int64_t cap = (int64_t)sm_count_cached() * occ;
     if (grid > cap) grid = cap;
-    k_batched<<<(unsigned)grid, B_WARPS * 32, 0, st>>>(X, norm ? X : Y, rows, len, ld, prm, values, counts, info);
+    kern<<<(unsigned)grid, B_WARPS * 32, 0, st>>>(X, Y, rows, len, ld, prm, values, counts, info);
     return cudaGetLastError();
 }
 
