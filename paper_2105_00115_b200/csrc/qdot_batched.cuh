@@ -110,16 +110,17 @@ __device__ __forceinline__ void b_cold_add(BWarp& W, int c, int64_t kd, int32_t 
 }
 
 // everything outside the private window: limb-table keys, zero / subnormal /
-// non-finite / extreme elements (limb table or a row flag)
-__device__ __noinline__ void b_cold(BWarp& W, int cbase, double xv, double yv, uint32_t* zc, uint32_t* st) {
+// non-finite / extreme elements (limb table or a row flag).  Returns the row
+// status bits it raises, plus 256 for a zero product.
+__device__ __noinline__ uint32_t b_cold(BWarp& W, int cbase, double xv, double yv) {
     uint64_t bx = dbits(xv), by = dbits(yv);
-    if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) { *st |= BS_NONFINITE; return; }
-    if (xv == 0.0 || yv == 0.0) { (*zc)++; return; }
+    if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) return BS_NONFINITE;
+    if (xv == 0.0 || yv == 0.0) return 256u;
     int e = flexp_bits(bx) + flexp_bits(by);
     int c = e + KOFF - cbase;
-    if ((unsigned)c >= (unsigned)BCW) { *st |= BS_GENERAL; return; }
+    if ((unsigned)c >= (unsigned)BCW) return BS_GENERAL;
     uint64_t pb = dbits(__dmul_rn(xv, yv));
-    if (((pb >> 52) & 0x7FF) == 0x7FF) { *st |= BS_GENERAL; return; }     // DOUBLE overflow: rare, general path
+    if (((pb >> 52) & 0x7FF) == 0x7FF) return BS_GENERAL;     // DOUBLE overflow: rare, general path
     int64_t kd = double_units(pb, e);
     int32_t ks, kh;
     exact_variants(bitsd(mant_bits(bx)), bitsd(mant_bits(by)), ks, kh);
@@ -127,34 +128,43 @@ __device__ __noinline__ void b_cold(BWarp& W, int cbase, double xv, double yv, u
     ks = (ks ^ sg) - sg;
     kh = (kh ^ sg) - sg;
     b_cold_add(W, c, kd, ks, kh);
+    return 0u;
 }
 
-// one element: private-window keys (both factors normal; the window lies in
-// e in [-971, 1021], so 2^(52-e) is representable and fl(x*y) normal) inline,
-// everything else through b_cold
-__device__ __forceinline__ void b_elem(BWarp& W, ulonglong2* __restrict__ my, int kbias, int cbase, double xv,
-                                       double yv, uint32_t* zc, uint32_t* st) {
-    const uint32_t hx = (uint32_t)(dbits(xv) >> 32), hy = (uint32_t)(dbits(yv) >> 32);
-    const uint32_t fx = (hx >> 20) & 0x7FFu, fy = (hy >> 20) & 0x7FFu;
-    const uint32_t esum = fx + fy;
-    const int rel = (int)esum + kbias;
-    if (((unsigned)rel < (unsigned)BW) & (max(fx - 1u, fy - 1u) < 0x7FEu)) {
-        const double scale = __hiloint2double((int)((3121u - esum) << 20), 0);   // 2^(52-e)
-        const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv, yv), scale));
-        const uint64_t bx = dbits(xv), by = dbits(yv);
-        int32_t ks, kh;
-        exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
-                       bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
-        const int32_t s32 = (int32_t)(hx ^ hy) >> 31;
-        ks = (ks ^ s32) - s32;
-        kh = (kh ^ s32) - s32;
-        ulonglong2* slot = my + rel * 32;
-        ulonglong2 v = *slot;
-        v.x += (unsigned long long)kd;
-        v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
-        *slot = v;
-    } else {
-        b_cold(W, cbase, xv, yv, zc, st);
+// NE elements of one lane.  Private-window keys (both factors normal; the
+// window lies in e in [-971, 1021], so 2^(52-e) is representable and fl(x*y)
+// normal) update their slot inline; the rest go through b_cold (rare).
+// ok: element in range (ragged tail).
+template <int NE>
+__device__ __forceinline__ void b_elems(BWarp& W, ulonglong2* __restrict__ my, int kbias, int cbase,
+                                        const double (&xv)[NE], const double (&yv)[NE], const bool (&ok)[NE],
+                                        uint32_t& zc, uint32_t& st) {
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+        const uint32_t hx = (uint32_t)(dbits(xv[j]) >> 32), hy = (uint32_t)(dbits(yv[j]) >> 32);
+        const uint32_t fx = (hx >> 20) & 0x7FFu, fy = (hy >> 20) & 0x7FFu;
+        const uint32_t esum = fx + fy;
+        const int rel = (int)esum + kbias;
+        if (((unsigned)rel < (unsigned)BW) & (max(fx - 1u, fy - 1u) < 0x7FEu) & ok[j]) {
+            const double scale = __hiloint2double((int)((3121u - esum) << 20), 0);   // 2^(52-e)
+            const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv[j], yv[j]), scale));
+            const uint64_t bx = dbits(xv[j]), by = dbits(yv[j]);
+            int32_t ks, kh;
+            exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
+                           bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
+            const int32_t s32 = (int32_t)(hx ^ hy) >> 31;
+            ks = (ks ^ s32) - s32;
+            kh = (kh ^ s32) - s32;
+            ulonglong2* slot = my + rel * 32;
+            ulonglong2 v = *slot;
+            v.x += (unsigned long long)kd;
+            v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
+            *slot = v;
+        } else if (ok[j]) {
+            const uint32_t r = b_cold(W, cbase, xv[j], yv[j]);
+            zc += r >> 8;
+            st |= r & 0xFFu;
+        }
     }
 }
 
@@ -227,7 +237,7 @@ __device__ __forceinline__ void b_load_tail(const double* __restrict__ xr, const
 }
 
 template <bool NORM, bool VEC>
-__global__ void __launch_bounds__(B_WARPS * 32)
+__global__ void __launch_bounds__(B_WARPS * 32, 5)
 k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows, int64_t len, int64_t ld,
           BParams prm, double* __restrict__ values, int64_t* __restrict__ counts, int32_t* __restrict__ info) {
     __shared__ BWarp warps[B_WARPS];
@@ -262,9 +272,9 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
                 k4[j] = (ok0[j] && fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) ? (int)(fx + fy) - 2046 + KOFF : -10000;
                 kmx = max(kmx, k4[j]);
             }
-            for (int o = 16; o; o >>= 1) kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
-            // window [kmax - W + 3, kmax + 2] when it holds >= 3/4 of the sample
-            int cand = kmx - BW + 3, cov = 0, nv = 0;
+            kmx = __reduce_max_sync(0xffffffffu, kmx);
+            // window [kmax - W + 2, kmax + 1] when it holds >= 3/4 of the sample
+            int cand = kmx - BW + 2, cov = 0, nv = 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 cov += __popc(__ballot_sync(0xffffffffu, (unsigned)(k4[j] - cand) < (unsigned)BW));
@@ -311,8 +321,8 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
                 if (it + 1 < nfull) b_load_full<NORM>(xr, yr, (it + 1) * 128, lane, nx, ny);
                 if (lane == 0 && (it & (B_CHUNK / 128 - 1)) == 0)
                     b_prefetch(xr, yr, xn, yn, len, it / (B_CHUNK / 128) + B_PFC, NORM);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) b_elem(W, my, kbias, cbase, cx[j], cy[j], &zc, &st);
+                const bool all[4] = {true, true, true, true};
+                b_elems<4>(W, my, kbias, cbase, cx, cy, all, zc, st);
                 if (++since == 62) { b_flush(W, lane, base - cbase); since = 0; }   // <= 248 elements per lane
             };
             int64_t it = 0;
@@ -325,18 +335,14 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
             for (int64_t i0 = it * 128; i0 < len; i0 += 128) {
                 bool ok[4];
                 b_load_tail<NORM>(xr, yr, i0, len, lane, xa, ya, ok);
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if (ok[j]) b_elem(W, my, kbias, cbase, xa[j], ya[j], &zc, &st);
+                b_elems<4>(W, my, kbias, cbase, xa, ya, ok, zc, st);
                 if (++since == 62) { b_flush(W, lane, base - cbase); since = 0; }
             }
             b_flush(W, lane, base - cbase);
         }
         // row-wide status and zero count
-        for (int o = 16; o; o >>= 1) {
-            st |= __shfl_xor_sync(0xffffffffu, st, o);
-            zc += __shfl_xor_sync(0xffffffffu, zc, o);
-        }
+        st = __reduce_or_sync(0xffffffffu, st);          // row length <= B_MAXLEN: 32-bit counts
+        zc = __reduce_add_sync(0xffffffffu, zc);
         double value = 0.0;
         long long cnt_p[4] = {0, 0, 0, 0};
         int nbins = 0, emin = 0, emax = 0;
@@ -369,7 +375,7 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
                 long long nnz = 0;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) nnz += cnt[h];
-                for (int o = 16; o; o >>= 1) nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+                nnz = __reduce_add_sync(0xffffffffu, (unsigned)nnz);
                 if (early) {
                     st |= BS_EARLY;
                     if (prm.input_mu != 52) st |= BS_GENERAL;
@@ -422,9 +428,8 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
                     }
                     value = (s - s == 0.0) ? __dadd_rn(s, c) : s;
                 }
-                for (int p = 0; p < 4; ++p)
-                    for (int o = 16; o; o >>= 1) cnt_p[p] += __shfl_xor_sync(0xffffffffu, cnt_p[p], o);
-                for (int o = 16; o; o >>= 1) st |= __shfl_xor_sync(0xffffffffu, st, o);
+                for (int p = 0; p < 4; ++p) cnt_p[p] = __reduce_add_sync(0xffffffffu, (unsigned)cnt_p[p]);
+                st = __reduce_or_sync(0xffffffffu, st);
             }
         }
         if (lane == 0) {
