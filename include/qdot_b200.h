@@ -64,7 +64,7 @@ typedef struct {
     int32_t split;           /* 0 = SplitMode.NONE, 1 = SplitMode.PER_BIN       */
     int32_t input_mu;        /* 52, 23 or 10                                    */
     int32_t strategy;        /* qdot_strategy                                   */
-    int32_t reserved;        /* pass-1 mode hint: 0 auto, 1 lean, 2 full        */
+    int32_t reserved;        /* pass-1 speed knob: see qdot_b200_pass1          */
     int64_t strategy_param;  /* width (ranged, >= 1) or levels (split, >= 0)    */
 } qdot_config;
 
@@ -132,8 +132,9 @@ int qdot_b200_begin(void* ws, void* stream);
  * binning.sorted_bin_init's histogram (binning.py:102-106) and, for every
  * bin whose products do not depend on the partition, emulate.bin_dot.
  * cfg (may be NULL) and n_total (elements over all ranks) only steer the
- * per-CTA lean/full choice (speed, never results); cfg->reserved = 0 auto,
- * 1 lean, 2 full. */
+ * per-CTA lean/full and cold-queue choices (speed, never results);
+ * cfg->reserved bits 0-1: 0 auto, 1 lean, 2 full; bits 2-3: cold-element warp
+ * queue 0 auto, 4 on, 8 off. */
 int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
                     int64_t n_total, void* ws, void* stream);
 /* one-CTA scoring on the (reduced) histogram: partition, scores, precisions.

@@ -45,9 +45,11 @@ struct __align__(16) P1Shared {
     uint32_t c_cnt[P1_CW], c_d0[P1_CW], c_d1[P1_CW], c_d2[P1_CW], c_d3[P1_CW];
     uint32_t c_s0[P1_CW], c_s1[P1_CW], c_h[P1_CW];
     unsigned long long red[2 * (P1_T / 32)];
+    double2 q[P1_T / 32][32];                // per-warp queue of cold elements (queue mode)
     int base;                                // first key of the private window
     int cbase;                               // first key of the cold window
     int full;                                // this CTA runs the full-variant loop
+    int queue;                               // this CTA compacts cold elements through the warp queue
     int kmax;                                // largest sampled key
 };
 
@@ -125,8 +127,10 @@ __device__ __noinline__ void p1_special(P1Shared& S, int64_t* __restrict__ A, in
 // one element.  Private-window elements (both factors normal, key in the
 // window, which lies inside e in [-971, 1021]): fl(x*y) * 2^(52-e) is an exact
 // integer in [2^52, 2^54] -> one conversion gives the signed DOUBLE units.
-template <bool FULL>
-__device__ __forceinline__ void p1_elem(P1Shared& S, ulonglong2* __restrict__ my, int kbias,
+// QUEUE: elements outside the private window are not handled here; the
+// return value flags them for the warp queue.
+template <bool FULL, bool QUEUE>
+__device__ __forceinline__ bool p1_elem(P1Shared& S, ulonglong2* __restrict__ my, int kbias,
                                         int64_t* __restrict__ A, int64_t* __restrict__ B, double xv, double yv,
                                         uint32_t* zc, uint32_t* nf) {
     const uint32_t hx = (uint32_t)(dbits(xv) >> 32), hy = (uint32_t)(dbits(yv) >> 32);
@@ -154,6 +158,8 @@ __device__ __forceinline__ void p1_elem(P1Shared& S, ulonglong2* __restrict__ my
             v.y = (unsigned long long)((uint32_t)v.y + 1u);   // count < 2^32 between flushes
         }
         *slot = v;
+    } else if (QUEUE) {
+        return true;
     } else if ((max(fx - 1u, fy - 1u) < 0x7FEu) & (esum - 1024u < 2044u)) {  // normal, e in [-1022, 1021]
         const uint64_t bx = dbits(xv), by = dbits(yv);
         const int e = (int)esum - 2046;
@@ -162,6 +168,50 @@ __device__ __forceinline__ void p1_elem(P1Shared& S, ulonglong2* __restrict__ my
                 (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)(hx ^ hy) >> 31);
     } else {
         p1_special(S, A, B, xv, yv, zc, nf);
+    }
+    return false;
+}
+
+// an element outside the private window (also the queue drain)
+__device__ __forceinline__ void p1_outside(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B,
+                                           double xv, double yv, uint32_t* zc, uint32_t* nf) {
+    const uint32_t hx = (uint32_t)(dbits(xv) >> 32), hy = (uint32_t)(dbits(yv) >> 32);
+    const uint32_t fx = (hx >> 20) & 0x7FFu, fy = (hy >> 20) & 0x7FFu;
+    const uint32_t esum = fx + fy;
+    if ((max(fx - 1u, fy - 1u) < 0x7FEu) & (esum - 1024u < 2044u)) {
+        const uint64_t bx = dbits(xv), by = dbits(yv);
+        const int e = (int)esum - 2046;
+        const int64_t kd = double_units(dbits(__dmul_rn(xv, yv)), e);
+        p1_cold(S, A, B, e + KOFF, kd, (bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull,
+                (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)(hx ^ hy) >> 31);
+    } else {
+        p1_special(S, A, B, xv, yv, zc, nf);
+    }
+}
+
+// process the warp's queued cold elements, one per lane (warp-collective)
+__device__ __forceinline__ void p1_drain(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B, int warp,
+                                         int lane, uint32_t& qn, uint32_t* zc, uint32_t* nf) {
+    __syncwarp();
+    if ((uint32_t)lane < qn) {
+        const double2 e = S.q[warp][lane];
+        p1_outside(S, A, B, e.x, e.y, zc, nf);
+    }
+    qn = 0;
+    __syncwarp();
+}
+
+// append this slot's cold elements (flag c per lane) to the warp queue,
+// draining whenever 32 entries would be exceeded (warp-collective)
+__device__ __forceinline__ void p1_enqueue(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B, int warp,
+                                           int lane, uint32_t& qn, bool c, double xv, double yv, uint32_t* zc,
+                                           uint32_t* nf) {
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    if (m) {
+        const uint32_t k = __popc(m);
+        if (qn + k > 32) p1_drain(S, A, B, warp, lane, qn, zc, nf);
+        if (c) S.q[warp][qn + __popc(m & ((1u << lane) - 1u))] = make_double2(xv, yv);
+        qn += k;
     }
 }
 
@@ -263,19 +313,25 @@ __device__ __forceinline__ void p1_load(const double* __restrict__ x, const doub
     }
 }
 
-template <bool FULL, int V>
+template <bool FULL, bool QUEUE, int V>
 __device__ __forceinline__ void p1_tile(P1Shared& S, ulonglong2* __restrict__ my, int kbias,
                                         int64_t* __restrict__ A, int64_t* __restrict__ B,
                                         const double (&xv)[2 * V], const double (&yv)[2 * V], int64_t e0,
-                                        int64_t n, bool fulltile, int tid, uint32_t* zc, uint32_t* nf) {
+                                        int64_t n, bool fulltile, int tid, uint32_t& qn, uint32_t* zc, uint32_t* nf) {
     if (fulltile) {
 #pragma unroll
-        for (int j = 0; j < 2 * V; ++j) p1_elem<FULL>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+        for (int j = 0; j < 2 * V; ++j) {
+            const bool c = p1_elem<FULL, QUEUE>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+            if (QUEUE) p1_enqueue(S, A, B, tid >> 5, tid & 31, qn, c, xv[j], yv[j], zc, nf);
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < 2 * V; ++j)
+        for (int j = 0; j < 2 * V; ++j) {
+            bool c = false;
             if (e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1) < n)
-                p1_elem<FULL>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+                c = p1_elem<FULL, QUEUE>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+            if (QUEUE) p1_enqueue(S, A, B, tid >> 5, tid & 31, qn, c, xv[j], yv[j], zc, nf);
+        }
     }
 }
 
@@ -292,7 +348,7 @@ __device__ __forceinline__ void p1_prefetch_l2(const double* x, const double* y,
 // persistent loop over tiles.  PF: register double buffering (the loads of
 // the CTA's next tile are in flight while the current one is processed).
 // L2D > 0: one thread per CTA bulk-prefetches the tile L2D+1 iterations ahead into L2.
-template <bool NORM, bool VEC, bool FULL, int V, bool PF, int L2D>
+template <bool NORM, bool VEC, bool FULL, bool QUEUE, int V, bool PF, int L2D>
 __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ x, const double* __restrict__ y,
                                         int64_t n, int64_t* __restrict__ A, int64_t* __restrict__ B, int tid,
                                         uint32_t* zc, uint32_t* nf) {
@@ -304,6 +360,11 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
     const int kbias = KOFF - 2046 - S.base;
     ulonglong2* __restrict__ my = S.priv + tid;
     int since = 0;
+    uint32_t qn = 0;                                   // warp queue fill (warp-uniform)
+    auto flush = [&]() {
+        if (QUEUE) p1_drain(S, A, B, tid >> 5, tid & 31, qn, zc, nf);
+        p1_flush<FULL>(S, A, B, tid);
+    };
     if (!PF) {
         if (L2D > 0 && tid == 0) {   // warm the first prefetch window
             for (int d = 1; d <= L2D; ++d) p1_prefetch_l2<NORM>(x, y, n, blockIdx.x + d * stride, TILE);
@@ -313,8 +374,8 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
             bool f;
             if (L2D > 0 && tid == 0) p1_prefetch_l2<NORM>(x, y, n, t + (L2D + 1) * stride, TILE);
             p1_load<NORM, VEC, V>(x, y, n, t, tid, xv, yv, f);
-            p1_tile<FULL, V>(S, my, kbias, A, B, xv, yv, t * TILE, n, f, tid, zc, nf);
-            if (++since == FLUSH) { p1_flush<FULL>(S, A, B, tid); since = 0; }
+            p1_tile<FULL, QUEUE, V>(S, my, kbias, A, B, xv, yv, t * TILE, n, f, tid, qn, zc, nf);
+            if (++since == FLUSH) { flush(); since = 0; }
         }
     } else {
         double xa[EPT], ya[EPT], xb[EPT], yb[EPT];
@@ -324,17 +385,17 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
         while (t < ntiles) {
             const int64_t tb = t + stride;
             if (tb < ntiles) p1_load<NORM, VEC, V>(x, y, n, tb, tid, xb, yb, fb);
-            p1_tile<FULL, V>(S, my, kbias, A, B, xa, ya, t * TILE, n, fa, tid, zc, nf);
-            if (++since == FLUSH) { p1_flush<FULL>(S, A, B, tid); since = 0; }
+            p1_tile<FULL, QUEUE, V>(S, my, kbias, A, B, xa, ya, t * TILE, n, fa, tid, qn, zc, nf);
+            if (++since == FLUSH) { flush(); since = 0; }
             if (tb >= ntiles) break;
             const int64_t ta = tb + stride;
             if (ta < ntiles) p1_load<NORM, VEC, V>(x, y, n, ta, tid, xa, ya, fa);
-            p1_tile<FULL, V>(S, my, kbias, A, B, xb, yb, tb * TILE, n, fb, tid, zc, nf);
-            if (++since == FLUSH) { p1_flush<FULL>(S, A, B, tid); since = 0; }
+            p1_tile<FULL, QUEUE, V>(S, my, kbias, A, B, xb, yb, tb * TILE, n, fb, tid, qn, zc, nf);
+            if (++since == FLUSH) { flush(); since = 0; }
             t = ta;
         }
     }
-    p1_flush<FULL>(S, A, B, tid);
+    flush();
 }
 
 template <bool NORM, bool VEC, int V, bool PF, int L2D>
@@ -431,8 +492,8 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
             S.cbase = cb;
             // lean / full decision (see header); only speed depends on it
             int full = 0;
-            if (prm.mode == 2 || prm.input_mu != 52) full = 1;
-            else if (prm.mode == 0) {
+            if ((prm.mode & 3) == 2 || prm.input_mu != 52) full = 1;
+            else if ((prm.mode & 3) == 0) {
                 const uint32_t ns = pref[KEYS];
                 const int fl = flexp_bits(dbits(prm.epsilon));
                 for (int r = 0; r < P1_W && ns; ++r) {
@@ -445,6 +506,9 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                 }
             }
             S.full = full;
+            // queue mode when more than 1/128 of the sample lies outside the private window
+            const uint32_t ns = pref[KEYS], cov = pref[b + P1_W] - pref[b];
+            S.queue = (prm.mode >> 2) == 1 ? 1 : ((prm.mode >> 2) == 2 ? 0 : ((ns - cov) * 128u > ns));
         }
     }
     __syncthreads();
@@ -460,8 +524,13 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     // ---- main streaming loop (persistent grid over tiles)
     uint32_t zc = 0, nf = 0;
     const bool fullmode = S.full != 0;
-    if (fullmode) p1_main<NORM, VEC, true, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
-    else p1_main<NORM, VEC, false, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
+    if (S.queue) {
+        if (fullmode) p1_main<NORM, VEC, true, true, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
+        else p1_main<NORM, VEC, false, true, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
+    } else {
+        if (fullmode) p1_main<NORM, VEC, true, false, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
+        else p1_main<NORM, VEC, false, false, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
+    }
 
     // ---- publish CTA partials (the cold table was pushed by the last flush)
     for (int r = tid; r < P1_W; r += P1_T) {

@@ -38,7 +38,7 @@ if iters:
         if e:
             b[round(e / iters, 2)] += e
     print("per-iteration multiplicity buckets:")
-    for k, v in sorted(b.items(), key=lambda kv: -kv[1])[:12]:
+    for k, v in sorted(((k, v) for k, v in b.items() if k > 0), key=lambda kv: -kv[1])[:12]:
         print(f"  x{k:7.3f}: {v / tot * 100:5.1f}% of instructions, {v / (k * iters):.0f} static instrs")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
