@@ -182,6 +182,20 @@ int qdot_b200_batched(const double* X, const double* Y, int64_t rows, int64_t le
 int qdot_b200_bin_ids(const double* x, const double* y, int64_t n, int norm, const int32_t* lut_bin,
                       int32_t* bin_ids, void* stream);
 
+/* --- solver callers (apps.py: acg / apm) -------------------------------------- */
+/* y = A x for a CSR matrix (int64 indptr[n_rows+1], int32 or int64 column
+ * indices: index_bytes 4 or 8).  Each row is summed sequentially from +0.0 in
+ * CSR order with separately rounded products, bit-identical to scipy's
+ * csr_matvec used by SparseMatrix.matvec (apps.py:57-58).  indices, data and x
+ * are only read through the row extents (may be NULL for an empty matrix). */
+int qdot_b200_csr_spmv(int64_t n_rows, const int64_t* indptr, const void* indices, int index_bytes,
+                       const double* data, const double* x, double* y, void* stream);
+/* elementwise vector updates of the solvers (apps.py:216-220, 306-308), each
+ * bit-identical to the numpy expression: op 0 out = a + s*b, op 1 out = a - s*b
+ * (s*b rounded first), op 2 out = a / s (b unused).  out may alias a or b. */
+int qdot_b200_vec_update(int64_t n, int op, const double* a, double s, const double* b, double* out,
+                         void* stream);
+
 /* --- host-side helpers (no GPU needed; exported for tests and bindings) ----- */
 /* correctly rounded acc * 2^u with math.ldexp semantics; *overflow set on range error */
 double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow);

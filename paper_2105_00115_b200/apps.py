@@ -1,0 +1,415 @@
+"""Iterative-solver callers of qdot, on the device: approximate CG (acg) and
+the approximate power method (apm).
+
+Mirrors the reference's apps.py (apps.py:1-359): same names, signatures,
+result types, trace schema and exceptions.  Underneath, every vector lives in
+HBM and every operation runs in this package's sm_100a kernels:
+
+    A.matvec(p)         qdot_b200_csr_spmv   (bit-identical to scipy csr_matvec)
+    x + alpha*p, ...    qdot_b200_vec_update (bit-identical to the numpy expression)
+    r.r, p.Ap, ...      the qdot device pipeline (bit-identical to kernel.qdot)
+
+so iterates, iteration counts, residuals and precision traces equal the
+reference's bit for bit.  Host work per iteration is the scalar recurrence
+(alpha = c/d, beta, sqrt) in Python floats, exactly as the reference does it.
+
+The generators (gen_stencil, gen_graph_laplacian) build the same CSR matrices
+as the reference on the host; they are input preparation, not the hot path.
+reference_cg / reference_pm are the plain-double baselines (torch on the
+device), kept for iteration-count comparisons like the reference's.
+"""
+
+from __future__ import annotations
+
+import csv
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import IO, List, Optional, Tuple, Union
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .binning import ExactBinning, Strategy
+from .device import require_cuda, stream_handle, thread_state
+from .kernel import _raise_status, run_device
+from .scoring import LEVELS_ASC, PrecisionLevel, SplitMode, ToleranceConfig
+
+__all__ = ["TRACE_HEADER", "BreakdownError", "ZeroIterateError", "SparseMatrix", "gen_stencil",
+           "gen_graph_laplacian", "TraceRow", "SolveTrace", "CGResult", "PMResult", "acg", "apm",
+           "reference_cg", "reference_pm"]
+
+TRACE_HEADER = "iter,call_site,pct_perforate,pct_half,pct_single,pct_double,resid_or_lambda"   # apps.py:22
+
+_ADD, _SUB, _DIV = 0, 1, 2
+
+
+class BreakdownError(RuntimeError):
+    """CG direction lost positive curvature (p.Ap <= 0 or non-finite)."""
+
+
+class ZeroIterateError(RuntimeError):
+    """Power-method iterate collapsed to the zero vector."""
+
+
+# --------------------------------------------------------------------------- device helpers
+def _dev():
+    torch = require_cuda()
+    return torch, torch.device("cuda", torch.cuda.current_device())
+
+
+def _to_device(v, n: Optional[int] = None):
+    torch, device = _dev()
+    if isinstance(v, torch.Tensor):
+        t = v.to(device=device, dtype=torch.float64).contiguous()
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(device)
+    if t.dim() != 1 or (n is not None and t.shape[0] != n):
+        raise ValueError(f"expected a 1-D vector of length {n}")
+    return t
+
+
+def _update(op: int, a, s: float, b, out) -> None:
+    """out = a + s*b | a - s*b | a / s on the device (numpy rounding)."""
+    lib = _lib.load()
+    _lib.check(lib.qdot_b200_vec_update(a.shape[0], op, a.data_ptr(), float(s),
+                                        b.data_ptr() if b is not None else None, out.data_ptr(),
+                                        stream_handle(a.device)), lib)
+
+
+class _Dots:
+    """qdot calls of one solver run: the device pipeline with a reused
+    workspace, returning what the solvers and their traces consume."""
+
+    def __init__(self, cfg: ToleranceConfig, strategy):
+        self.cfg, self.strategy = cfg, strategy
+
+    def __call__(self, xd, yd, norm: bool):
+        n = int(xd.shape[0])
+        res, _, _ = run_device(xd, xd if norm else yd, n, norm, self.cfg, self.strategy, timing=False)
+        _raise_status(res)
+        counts = {level: int(res.counts[i]) for i, level in enumerate(LEVELS_ASC)}
+        return _DotReport(float(res.value), counts, n, int(res.zero_count))
+
+
+@dataclass
+class _DotReport:
+    """The QdotReport fields a solver trace reads (value, counts, n)."""
+
+    value: float
+    counts: dict
+    n: int
+    zero_count: int
+
+
+# --------------------------------------------------------------------------- matrices
+@dataclass
+class SparseMatrix:
+    """CSR storage plus the symmetry promise the solvers rely on (apps.py:33-58);
+    a device copy (int64 indptr, int32/int64 indices, fp64 data) is made on
+    first use."""
+
+    indptr: np.ndarray
+    indices: np.ndarray
+    data: np.ndarray
+    n: int
+    symmetric: bool = True
+    _csr: Optional[sp.csr_matrix] = field(default=None, repr=False, compare=False)
+    _device: Optional[tuple] = field(default=None, repr=False, compare=False)
+
+    @classmethod
+    def from_csr(cls, m: sp.csr_matrix, symmetric: bool = True) -> "SparseMatrix":
+        m = m.tocsr()
+        m.sort_indices()
+        return cls(indptr=m.indptr, indices=m.indices, data=m.data, n=m.shape[0], symmetric=symmetric, _csr=m)
+
+    def csr(self) -> sp.csr_matrix:
+        if self._csr is None:
+            self._csr = sp.csr_matrix((self.data, self.indices, self.indptr), shape=(self.n, self.n))
+        return self._csr
+
+    def device_arrays(self):
+        if self._device is None:
+            torch, device = _dev()
+            indptr = torch.from_numpy(np.ascontiguousarray(self.indptr, dtype=np.int64)).to(device)
+            idx = np.ascontiguousarray(self.indices)
+            if idx.dtype not in (np.int32, np.int64):
+                idx = idx.astype(np.int64)
+            indices = torch.from_numpy(idx).to(device)
+            data = torch.from_numpy(np.ascontiguousarray(self.data, dtype=np.float64)).to(device)
+            self._device = (indptr, indices, int(idx.dtype.itemsize), data)
+        return self._device
+
+    def matvec_device(self, xd, out=None):
+        """y = A x with device vectors (qdot_b200_csr_spmv)."""
+        torch, _ = _dev()
+        indptr, indices, ib, data = self.device_arrays()
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.float64, device=xd.device)
+        lib = _lib.load()
+        _lib.check(lib.qdot_b200_csr_spmv(self.n, indptr.data_ptr(), indices.data_ptr(), ib, data.data_ptr(),
+                                          xd.data_ptr(), out.data_ptr(), stream_handle(xd.device)), lib)
+        return out
+
+    def matvec(self, v):
+        """A v on the device; numpy in -> numpy out, tensor in -> tensor out."""
+        torch, _ = _dev()
+        out = self.matvec_device(_to_device(v, self.n))
+        return out if isinstance(v, torch.Tensor) else out.cpu().numpy()
+
+
+def gen_stencil(nx: int, ny: int, nz: int) -> Tuple[SparseMatrix, np.ndarray]:
+    """27-point stencil on an nx*ny*nz grid (apps.py:61-91): diagonal 27,
+    in-grid neighbours -1; rhs = row sums, so the exact solution is all ones."""
+    if nx < 1 or ny < 1 or nz < 1:
+        raise ValueError("grid dimensions must be >= 1")
+    n = nx * ny * nz
+    gx, gy, gz = (a.ravel() for a in np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"))
+    point = (gx * ny + gy) * nz + gz
+    r_parts, c_parts, v_parts = [], [], []
+    for off in np.ndindex(3, 3, 3):
+        d = np.array(off) - 1
+        hx, hy, hz = gx + d[0], gy + d[1], gz + d[2]
+        inside = (hx >= 0) & (hx < nx) & (hy >= 0) & (hy < ny) & (hz >= 0) & (hz < nz)
+        r_parts.append(point[inside])
+        c_parts.append(((hx * ny + hy) * nz + hz)[inside])
+        v_parts.append(np.full(int(inside.sum()), 27.0 if not d.any() else -1.0))
+    m = sp.coo_matrix((np.concatenate(v_parts), (np.concatenate(r_parts), np.concatenate(c_parts))),
+                      shape=(n, n)).tocsr()
+    a = SparseMatrix.from_csr(m, symmetric=True)
+    rhs = a.csr() @ np.ones(n)           # host-side input preparation, as apps.py:90
+    return a, rhs
+
+
+def gen_graph_laplacian(n: int, edge_prob: float, seed: int = 0) -> SparseMatrix:
+    """Laplacian D - A of an Erdos-Renyi G(n, edge_prob) graph (apps.py:94-118):
+    the upper-triangle edges of row i are the draws rng.random(n-i-1) < p."""
+    if not (0.0 <= edge_prob <= 1.0):
+        raise ValueError("edge_prob must lie in [0, 1]")
+    if n < 1:
+        raise ValueError("n must be positive")
+    rng = np.random.default_rng(seed)
+    src, dst = [], []
+    for i in range(n - 1):
+        j = i + 1 + np.flatnonzero(rng.random(n - i - 1) < edge_prob)
+        src.append(np.full(j.size, i, dtype=np.int64))
+        dst.append(j)
+    r = np.concatenate(src) if src else np.empty(0, dtype=np.int64)
+    c = np.concatenate(dst) if dst else np.empty(0, dtype=np.int64)
+    adj = sp.coo_matrix((np.ones(r.size), (r, c)), shape=(n, n))
+    adj = adj + adj.T
+    deg = np.asarray(adj.sum(axis=1)).ravel()
+    return SparseMatrix.from_csr((sp.diags(deg) - adj).tocsr(), symmetric=True)
+
+
+# --------------------------------------------------------------------------- traces
+@dataclass
+class TraceRow:
+    iteration: int
+    call_site: str
+    counts: dict
+    n: int
+    resid_or_lambda: float
+
+    def pct(self, level: PrecisionLevel) -> float:
+        return 100.0 * self.counts.get(level, 0) / self.n if self.n else 0.0
+
+
+@dataclass
+class SolveTrace:
+    """Per-call precision mix of a solve (apps.py:134-159)."""
+
+    rows: List[TraceRow] = field(default_factory=list)
+
+    def record(self, iteration: int, call_site: str, report, resid_or_lambda: float) -> None:
+        self.rows.append(TraceRow(iteration, call_site, dict(report.counts), report.n, resid_or_lambda))
+
+    def write_csv(self, out: Union[str, IO[str]]) -> None:
+        own = isinstance(out, str)
+        fh = open(out, "w", newline="") if own else out
+        try:
+            fh.write(TRACE_HEADER + "\n")
+            w = csv.writer(fh, lineterminator="\n")
+            for r in self.rows:
+                w.writerow([r.iteration, r.call_site, repr(r.pct(PrecisionLevel.PERFORATE)),
+                            repr(r.pct(PrecisionLevel.HALF)), repr(r.pct(PrecisionLevel.SINGLE)),
+                            repr(r.pct(PrecisionLevel.DOUBLE)), repr(r.resid_or_lambda)])
+        finally:
+            if own:
+                fh.close()
+
+
+@dataclass
+class CGResult:
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    residual_norm: float
+    trace: SolveTrace
+
+
+@dataclass
+class PMResult:
+    eigenvalue: float
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    trace: SolveTrace
+
+
+# --------------------------------------------------------------------------- solvers
+def _norm_dot(dots: _Dots, v):
+    rep = dots(v, v, True)
+    if not (rep.value >= 0.0):                              # apps.py:171-175
+        raise AssertionError("norm computed by qdot must be nonnegative")
+    return rep
+
+
+def acg(a: SparseMatrix, b, x0=None, tau: float = 1e-8, epsilon: float = 1e-8,
+        split: SplitMode = SplitMode.PER_BIN, max_iters: int = 10_000, strategy: Strategy = None) -> CGResult:
+    """Conjugate gradient with r.r and p.Ap computed by qdot (apps.py:178-229)."""
+    if strategy is None:
+        strategy = ExactBinning()
+    if not a.symmetric:
+        raise ValueError("CG needs a symmetric positive definite matrix")
+    cfg = ToleranceConfig(epsilon=epsilon, split=split)
+    torch, device = _dev()
+    n = a.n
+    dots = _Dots(cfg, strategy)
+    x = torch.zeros(n, dtype=torch.float64, device=device) if x0 is None else _to_device(x0, n).clone()
+    bd = _to_device(b, n)
+    trace = SolveTrace()
+
+    q = a.matvec_device(x)
+    r = torch.empty_like(bd)
+    _update(_SUB, bd, 1.0, q, r)                              # r = b - A x (1.0 * q is exact)
+    p = r.clone()
+    c_rep = _norm_dot(dots, r)
+    c = c_rep.value
+    resid = math.sqrt(c)
+    trace.record(0, "rtr", c_rep, resid)
+
+    k = 0
+    while resid > tau and k < max_iters:
+        a.matvec_device(p, out=q)
+        d_rep = dots(p, q, False)
+        d = d_rep.value
+        if not math.isfinite(d) or d <= 0.0:
+            raise BreakdownError(f"p.Ap = {d!r} at iteration {k}")
+        alpha = c / d
+        _update(_ADD, x, alpha, p, x)                         # x = x + alpha * p
+        _update(_SUB, r, alpha, q, r)                         # r = r - alpha * q
+        c_rep = _norm_dot(dots, r)
+        c_new = c_rep.value
+        beta = c_new / c
+        _update(_ADD, r, beta, p, p)                          # p = r + beta * p
+        c = c_new
+        resid = math.sqrt(c)
+        k += 1
+        trace.record(k, "pAp", d_rep, resid)
+        trace.record(k, "rtr", c_rep, resid)
+    return CGResult(x=x.cpu().numpy(), iterations=k, converged=resid <= tau, residual_norm=resid, trace=trace)
+
+
+def apm(a: SparseMatrix, x0, tau: float = 1e-6, epsilon: float = 1e-7, split: SplitMode = SplitMode.PER_BIN,
+        max_iters: int = 300, strategy: Strategy = None) -> PMResult:
+    """Power method with z.z and the Rayleigh quotient computed by qdot (apps.py:275-325)."""
+    if strategy is None:
+        strategy = ExactBinning()
+    cfg = ToleranceConfig(epsilon=epsilon, split=split)
+    x_h = np.array(x0, dtype=np.float64)
+    nrm = float(np.linalg.norm(x_h))                          # host, as apps.py:292
+    if nrm == 0.0:
+        raise ZeroIterateError("x0 is the zero vector")
+    x = _to_device(x_h / nrm, a.n)
+    torch, _ = _dev()
+    dots = _Dots(cfg, strategy)
+    trace = SolveTrace()
+    z = torch.empty_like(x)
+    x_next = torch.empty_like(x)
+
+    lam_prev = None
+    lam = 0.0
+    k = 0
+    converged = False
+    while k < max_iters:
+        a.matvec_device(x, out=z)
+        # np.any(z) (apps.py:305) from the same qdot call: z.z has a zero
+        # product exactly where z_i == 0 (NaN makes qdot raise ValueError, as
+        # the reference's qdot would right after its np.any)
+        c_rep = _norm_dot(dots, z)
+        if c_rep.zero_count == c_rep.n:
+            raise ZeroIterateError(f"A x vanished at iteration {k}")
+        c = c_rep.value
+        s = math.sqrt(c)
+        _update(_DIV, z, s, None, x_next)                     # x_next = z / s
+        lam_rep = dots(x, x_next, False)
+        lam = lam_rep.value * s
+        k += 1
+        trace.record(k, "norm", c_rep, lam)
+        trace.record(k, "lambda", lam_rep, lam)
+        x, x_next = x_next, x
+        if lam_prev is not None and abs(lam - lam_prev) <= tau:
+            converged = True
+            break
+        lam_prev = lam
+    return PMResult(eigenvalue=lam, x=x.cpu().numpy(), iterations=k, converged=converged, trace=trace)
+
+
+def reference_cg(a: SparseMatrix, b, x0=None, tau: float = 1e-8, max_iters: int = 10_000) -> CGResult:
+    """Plain double CG with the identical stopping rule (apps.py:232-263), on
+    the device with torch dots (a baseline, not bit-identical to numpy's)."""
+    torch, device = _dev()
+    n = a.n
+    x = torch.zeros(n, dtype=torch.float64, device=device) if x0 is None else _to_device(x0, n).clone()
+    r = _to_device(b, n) - a.matvec_device(x)
+    p = r.clone()
+    c = float(torch.dot(r, r))
+    resid = math.sqrt(c)
+    k = 0
+    while resid > tau and k < max_iters:
+        q = a.matvec_device(p)
+        d = float(torch.dot(p, q))
+        if not math.isfinite(d) or d <= 0.0:
+            raise BreakdownError(f"p.Ap = {d!r} at iteration {k}")
+        alpha = c / d
+        x = x + alpha * p
+        r = r - alpha * q
+        c_new = float(torch.dot(r, r))
+        beta = c_new / c
+        p = r + beta * p
+        c = c_new
+        resid = math.sqrt(c)
+        k += 1
+    return CGResult(x=x.cpu().numpy(), iterations=k, converged=resid <= tau, residual_norm=resid,
+                    trace=SolveTrace())
+
+
+def reference_pm(a: SparseMatrix, x0, tau: float = 1e-6, max_iters: int = 300) -> PMResult:
+    """Plain double power method with the identical stopping rule (apps.py:328-359)."""
+    torch, _ = _dev()
+    x_h = np.array(x0, dtype=np.float64)
+    nrm = float(np.linalg.norm(x_h))
+    if nrm == 0.0:
+        raise ZeroIterateError("x0 is the zero vector")
+    x = _to_device(x_h / nrm, a.n)
+    lam_prev = None
+    lam = 0.0
+    k = 0
+    converged = False
+    while k < max_iters:
+        z = a.matvec_device(x)
+        if not bool(torch.any(z != 0)):
+            raise ZeroIterateError(f"A x vanished at iteration {k}")
+        c = float(torch.dot(z, z))
+        s = math.sqrt(c)
+        x_next = z / s
+        lam = float(torch.dot(x, x_next)) * s
+        k += 1
+        x = x_next
+        if lam_prev is not None and abs(lam - lam_prev) <= tau:
+            converged = True
+            break
+        lam_prev = lam
+    return PMResult(eigenvalue=lam, x=x.cpu().numpy(), iterations=k, converged=converged, trace=SolveTrace())

@@ -56,6 +56,11 @@ constexpr int FIRST_BINS = 64;
 
 }  // namespace
 
+namespace qd {
+// error reporting for the other translation units of the library
+int report_cuda_error(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+}  // namespace qd
+
 extern "C" {
 
 int qdot_b200_version(void) { return QDOT_B200_VERSION; }
