@@ -196,6 +196,34 @@ int qdot_b200_csr_spmv(int64_t n_rows, const int64_t* indptr, const void* indice
 int qdot_b200_vec_update(int64_t n, int op, const double* a, double s, const double* b, double* out,
                          void* stream);
 
+/* --- exact dot product (verification oracle) --------------------------------- */
+/* Correctly rounded x.y computed exactly on the device: the device form of
+ * kernel.reference_dot (kernel.py:98-133) for checking qdot at sizes the host
+ * cannot hold.  Every product is an exact integer mx*my * 2^(qx+qy); the pass
+ * sums them per exponent in integer limbs, finalize rounds once.  Sequence:
+ *   exact_begin -> exact_accumulate (per chunk / shard) [-> allreduce(SUM) of
+ *   the first qdot_b200_exact_region_words() int64 words of xws across ranks]
+ *   -> exact_plain (optional, serial) -> exact_finalize -> exact_fetch. */
+typedef struct {
+    double value;           /* correctly rounded dot product                         */
+    double plain;           /* left-to-right double sum of fl(x_i*y_i) (ReferenceResult.plain) */
+    int64_t nonfinite;      /* non-finite input elements (-> ValueError)             */
+    int32_t status;         /* QDOT_OK, QDOT_ERR_NONFINITE, QDOT_ERR_OVERFLOW        */
+    int32_t flexp_e;        /* flexp(value) when value != 0                          */
+    int32_t is_zero;        /* value == 0 (flexp_e undefined -> None)                */
+    int32_t fallback;       /* the reference would take its Fraction path            */
+    int32_t reserved[4];
+} qdot_exact_result;
+size_t qdot_b200_exact_workspace_bytes(void);
+int64_t qdot_b200_exact_region_words(void);
+int qdot_b200_exact_begin(void* xws, void* stream);
+int qdot_b200_exact_accumulate(const double* x, const double* y, int64_t n, int norm, void* xws, void* stream);
+/* one-thread sequential sum, chained across calls in element order; run after
+ * every exact_accumulate of the same vectors (its start value depends on them) */
+int qdot_b200_exact_plain(const double* x, const double* y, int64_t n, int norm, void* xws, void* stream);
+int qdot_b200_exact_finalize(void* xws, void* stream);
+int qdot_b200_exact_fetch(const void* xws, qdot_exact_result* out, void* stream);
+
 /* --- host-side helpers (no GPU needed; exported for tests and bindings) ----- */
 /* correctly rounded acc * 2^u with math.ldexp semantics; *overflow set on range error */
 double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow);

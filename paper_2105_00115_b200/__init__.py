@@ -9,7 +9,7 @@ include/qdot_b200.h (lib/libqdot_b200.so).  No CPU fallback.
 from .binning import (Bin, BinPartition, BinSplitting, ExactBinning, RangedBinning, Strategy,
                       parse_strategy, strategy_label)
 from .batched import BatchedReport, qdot_batched
-from .kernel import QdotReport, qdot, select_parameters
+from .kernel import QdotReport, ReferenceResult, qdot, reference_dot, select_parameters
 from .scoring import (ParameterSet, PrecisionLevel, SplitMode, ToleranceConfig, bin_score, ceil_log2,
                       early_termination, floor_log2, precision_of)
 
@@ -17,7 +17,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Bin", "BinPartition", "BinSplitting", "ExactBinning", "RangedBinning", "Strategy",
-    "parse_strategy", "strategy_label", "QdotReport", "qdot", "select_parameters",
+    "parse_strategy", "strategy_label", "QdotReport", "qdot", "select_parameters", "ReferenceResult", "reference_dot",
     "BatchedReport", "qdot_batched",
     "ParameterSet", "PrecisionLevel", "SplitMode", "ToleranceConfig", "bin_score", "ceil_log2",
     "early_termination", "floor_log2", "precision_of",

@@ -41,6 +41,12 @@ class QdotResult(ctypes.Structure):
                 ("reserved", ctypes.c_int32 * 5)]
 
 
+class QdotExactResult(ctypes.Structure):
+    _fields_ = [("value", ctypes.c_double), ("plain", ctypes.c_double), ("nonfinite", ctypes.c_int64),
+                ("status", ctypes.c_int32), ("flexp_e", ctypes.c_int32), ("is_zero", ctypes.c_int32),
+                ("fallback", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+
+
 class QdotWsLayout(ctypes.Structure):
     _fields_ = [("total_bytes", ctypes.c_int64), ("a_offset", ctypes.c_int64), ("a_len", ctypes.c_int64),
                 ("b_offset", ctypes.c_int64), ("b_len", ctypes.c_int64),
@@ -77,6 +83,13 @@ SIGNATURES = {
     "qdot_b200_batched": (_I, [_P, _P, _I64, _I64, _I64, _I, ctypes.POINTER(QdotConfig), _P, _P, _P, _P]),
     "qdot_b200_ldexp_rn": (ctypes.c_double, [ctypes.c_double, _I64, ctypes.POINTER(_I)]),
     "qdot_b200_csr_spmv": (_I, [_I64, _P, _P, _I, _P, _P, _P, _P]),
+    "qdot_b200_exact_workspace_bytes": (ctypes.c_size_t, []),
+    "qdot_b200_exact_region_words": (_I64, []),
+    "qdot_b200_exact_begin": (_I, [_P, _P]),
+    "qdot_b200_exact_accumulate": (_I, [_P, _P, _I64, _I, _P, _P]),
+    "qdot_b200_exact_plain": (_I, [_P, _P, _I64, _I, _P, _P]),
+    "qdot_b200_exact_finalize": (_I, [_P, _P]),
+    "qdot_b200_exact_fetch": (_I, [_P, ctypes.POINTER(QdotExactResult), _P]),
     "qdot_b200_vec_update": (_I, [_I64, _I, _P, ctypes.c_double, _P, _P, _P]),
 }
 

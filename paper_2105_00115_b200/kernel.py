@@ -27,10 +27,11 @@ import numpy as np
 from . import _lib
 from .binning import Bin, ExactBinning, Strategy, strategy_label
 from .device import as_device_vector, config_struct, require_cuda, stream_handle, thread_state
+from .exact import ReferenceResult, reference_dot  # noqa: F401  (kernel.py:75-133 live here in the reference)
 from .scoring import (ParameterSet, PrecisionLevel, SplitMode, ToleranceConfig, absolute_bound_term,
                       relative_bound_term)
 
-__all__ = ["QdotReport", "qdot", "select_parameters", "run_device"]
+__all__ = ["QdotReport", "qdot", "select_parameters", "run_device", "ReferenceResult", "reference_dot"]
 
 
 @dataclass
