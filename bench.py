@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--norm", action="store_true", help="norm mode x.x (8 B/elem)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the read probe and the C4 batched line")
     return ap.parse_args()
 
 
@@ -163,6 +164,60 @@ def cpu_baseline(n_sample: int, steps: int = 1):
     return {"value": n_sample / best, "unit": "elements/s", "cores": threads, "kind": "port",
             "sample": f"qdot n={n_sample} standard-normal eps=1e-8 exact, oracle/qdot_oracle.c, "
                       f"best of {len(times)}"}
+
+
+def measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, norm, Q, config_struct):
+    """Context numbers next to the headline: the HBM read ceiling of pass 1's
+    load pattern on the same 4 GiB (qdot_b200_read_probe), and BASELINE
+    configs[3] (C4: batched qdot, 65,536 rows x 4,096, eps 1e-6) timed with
+    CUDA events on device-resident inputs (4 GiB > L2)."""
+    import ctypes
+    s = stream.cuda_stream
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    vecs = [xd] if norm else [xd, yd]
+    for _ in range(2):
+        for v in vecs:
+            _lib.check(lib.qdot_b200_read_probe(v.data_ptr(), n, out.data_ptr(), s), lib)
+    reps = 10
+    e0.record(stream)
+    for _ in range(reps):
+        for v in vecs:
+            _lib.check(lib.qdot_b200_read_probe(v.data_ptr(), n, out.data_ptr(), s), lib)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    probe_ms = e0.elapsed_time(e1) / reps
+    res = {"read_probe": {"GBps": n * 8 * len(vecs) / (probe_ms * 1e-3) / 1e9, "ms": probe_ms,
+                          "bytes": n * 8 * len(vecs)}}
+    R, L = 65536, 4096
+    g = torch.Generator(device=dev).manual_seed(0)
+    X = torch.randn(R, L, dtype=torch.float64, device=dev, generator=g)
+    Y = torch.randn(R, L, dtype=torch.float64, device=dev, generator=g)
+    c = config_struct(Q.ToleranceConfig(1e-6), Q.ExactBinning())
+    vals = torch.empty(R, dtype=torch.float64, device=dev)
+    cnt = torch.empty((R, 4), dtype=torch.int64, device=dev)
+    info = torch.empty((R, 4), dtype=torch.int32, device=dev)
+
+    def run():
+        _lib.check(lib.qdot_b200_batched(X.data_ptr(), Y.data_ptr(), R, L, L, 0, ctypes.byref(c), vals.data_ptr(),
+                                         cnt.data_ptr(), info.data_ptr(), s), lib)
+    for _ in range(3):
+        run()
+    reps = 10
+    e0.record(stream)
+    for _ in range(reps):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    bms = e0.elapsed_time(e1) / reps
+    general = int(((info[:, 3] & 8) != 0).sum())
+    res["batched_c4"] = {"workload": "BASELINE configs[3]: 65,536 x 4,096 fp64 standard-normal, eps 1e-6, exact",
+                         "kernel": "qd::k_batched", "ms": bms, "dots_per_s": R / (bms * 1e-3),
+                         "elements_per_s": R * L / (bms * 1e-3),
+                         "GBps": R * L * 16 / (bms * 1e-3) / 1e9, "general_rows": general}
+    del X, Y
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_reference(args, rank, world):
@@ -332,6 +387,11 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "kernel": "qd::k_pass1",
                 "algorithmic_bytes_per_launch": n * bytes_per_elem, "kernel_ms": p1_ms,
                 "peak_kind": peak_kind, "kernel_share_of_step": p1_ms / ms}
+    secondary = None
+    if not args.no_secondary:
+        secondary = measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, args.norm, Q, config_struct)
+        roofline["read_probe_gbs"] = secondary["read_probe"]["GBps"]
+        roofline["frac_of_read_probe"] = achieved / secondary["read_probe"]["GBps"]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_sample)
@@ -353,6 +413,7 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

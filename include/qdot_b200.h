@@ -224,6 +224,11 @@ int qdot_b200_exact_plain(const double* x, const double* y, int64_t n, int norm,
 int qdot_b200_exact_finalize(void* xws, void* stream);
 int qdot_b200_exact_fetch(const void* xws, qdot_exact_result* out, void* stream);
 
+/* --- measurement ------------------------------------------------------------- */
+/* stream n doubles (16-byte aligned) once with pass 1's load pattern and
+ * discard them: the HBM read ceiling bench.py reports next to the copy peak */
+int qdot_b200_read_probe(const double* x, int64_t n, double* out, void* stream);
+
 /* --- host-side helpers (no GPU needed; exported for tests and bindings) ----- */
 /* correctly rounded acc * 2^u with math.ldexp semantics; *overflow set on range error */
 double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow);
