@@ -19,5 +19,12 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ex
    -o gpurun_out/exact_$TAG python scripts/exact_time.py > gpurun_out/ncu_exact_$TAG.log 2>&1
 timeout 300 python scripts/exact_time.py > gpurun_out/exact_time_$TAG.json 2>&1
 timeout 300 python scripts/latency.py > gpurun_out/latency_$TAG.jsonl 2>&1
+# summarise every capture here (ncu is on the box) and keep only the reports named in KEEP
+# (gpurun copies back at most 64 MiB)
+for rep in pass1 batched c3pass1 exact; do
+  [ -f gpurun_out/${rep}_$TAG.ncu-rep ] && python tools/ncu_summary.py gpurun_out/${rep}_$TAG.ncu-rep gpurun_out/${rep}_${TAG}_ncu > /dev/null 2>&1
+  case " ${KEEP:-batched} " in *" $rep "*) ;; *) rm -f gpurun_out/${rep}_$TAG.ncu-rep ;; esac
+done
+[ -f gpurun_out/launches_$TAG.csv ] && python tools/ncu_summary.py --launches gpurun_out/launches_$TAG.csv gpurun_out/launches_$TAG > /dev/null 2>&1
 tail -3 gpurun_out/pytest_$TAG.log; cat gpurun_out/bench_$TAG.json gpurun_out/exact_time_$TAG.json
 echo done
