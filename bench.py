@@ -290,6 +290,8 @@ def main():
     ev_p1 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
              for _ in range(args.steps)]
 
+    score_fn = lib.qdot_b200_score_finalize if world == 1 else lib.qdot_b200_score
+
     def step(i=None):
         _lib.check(lib.qdot_b200_begin(ws, s), lib)
         if i is not None:
@@ -299,7 +301,8 @@ def main():
             ev_p1[i][1].record(stream)
         if world > 1:
             reduce_regions(ra)                       # NCCL SUM of region A (histogram)
-        _lib.check(lib.qdot_b200_score(ws, n_total, ctypes.byref(c), s), lib)
+        # one GPU: score also finalizes (no pass 2 here); N > 1: finalize after allreduce(B)
+        _lib.check(score_fn(ws, n_total, ctypes.byref(c), s), lib)
         _lib.check(lib.qdot_b200_pass2(xp, yp, n, norm, ws, s), lib)
         if world > 1:
             reduce_regions(rb)                       # NCCL SUM of region B (exact partials)

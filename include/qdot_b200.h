@@ -141,6 +141,11 @@ int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const
  * Replaces kernel.select_parameters' partition + scoring (kernel.py:59-72,
  * binning.py:191-284, scoring.py:126-216).  n_total = elements over all ranks. */
 int qdot_b200_score(void* ws, int64_t n_total, const qdot_config* cfg, void* stream);
+/* single-device form of qdot_b200_score: when no pass 2 is needed (the common
+ * case) the same launch also runs finalize, and the later qdot_b200_pass2 /
+ * qdot_b200_finalize calls return on the device at once.  Not for multi-rank
+ * runs, whose finalize must follow the allreduce of region B. */
+int qdot_b200_score_finalize(void* ws, int64_t n_total, const qdot_config* cfg, void* stream);
 /* pass 2 (exits on the device unless score flagged it): scaled HALF/SINGLE
  * products for bins whose upper bound differs from the element's exponent
  * sum (ranged / split / early-terminated bins; emulate.py:137-153). */

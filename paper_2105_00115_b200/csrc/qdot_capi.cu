@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <vector>
 
 #include "qdot_common.cuh"
@@ -137,14 +138,22 @@ int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const
     return QDOT_OK;
 }
 
-int qdot_b200_score(void* ws, int64_t n_total, const qdot_config* cfg, void* stream) {
+static int score_impl(void* ws, int64_t n_total, const qdot_config* cfg, bool fuse, void* stream) {
     if (!ws || n_total < 0) return QDOT_ERR_ARG;
     int v = validate(cfg);
     if (v) return v;
     WsPtrs w = ws_ptrs(ws);
-    QD_CHECK(launch_score(w.a, w.lut_bin, w.lut_p2, w.meta, w.result, w.bins, n_total, *cfg,
+    QD_CHECK(launch_score(w.a, w.b, w.lut_bin, w.lut_p2, w.meta, w.result, w.bins, n_total, *cfg, fuse,
                           static_cast<cudaStream_t>(stream)), "score");
     return QDOT_OK;
+}
+
+int qdot_b200_score(void* ws, int64_t n_total, const qdot_config* cfg, void* stream) {
+    return score_impl(ws, n_total, cfg, false, stream);
+}
+
+int qdot_b200_score_finalize(void* ws, int64_t n_total, const qdot_config* cfg, void* stream) {
+    return score_impl(ws, n_total, cfg, true, stream);
 }
 
 int qdot_b200_pass2(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream) {
@@ -184,17 +193,151 @@ int qdot_b200_fetch(const void* ws, qdot_result* out, qdot_bin* bins, int32_t ma
     return QDOT_OK;
 }
 
+// ---- one-call path: a CUDA graph per (x, y, n, norm, cfg, ws, device), cached per
+// host thread, whose last node publishes the result block into host-mapped
+// memory; the host spins on its sequence word instead of a memcpy + sync.
+namespace {
+
+constexpr int PUBLISH_BYTES = 256 + (int)sizeof(qdot_bin) * FIRST_BINS;   // header + first bins
+constexpr int GRAPH_CACHE = 16;
+
+struct GraphKey {
+    const double* x;
+    const double* y;
+    int64_t n;
+    int norm;
+    int dev;
+    void* ws;
+    qdot_config cfg;
+    bool operator==(const GraphKey& o) const {
+        return x == o.x && y == o.y && n == o.n && norm == o.norm && dev == o.dev && ws == o.ws &&
+               std::memcmp(&cfg, &o.cfg, sizeof(cfg)) == 0;
+    }
+};
+
+struct FastState {
+    int dev = -1;
+    unsigned char* host = nullptr;      // mapped: [0, PUBLISH_BYTES) block, then the sequence word
+    unsigned char* host_dev = nullptr;
+    uint32_t* dev_seq = nullptr;
+    uint32_t expected = 0;
+    cudaStream_t cap = nullptr;
+    struct Entry { GraphKey k; cudaGraphExec_t exec; uint64_t use; };
+    std::vector<Entry> cache;
+    uint64_t tick = 0;
+    void clear() {
+        for (auto& e : cache) cudaGraphExecDestroy(e.exec);
+        cache.clear();
+        if (cap) cudaStreamDestroy(cap);
+        if (dev_seq) cudaFree(dev_seq);
+        if (host) cudaFreeHost(host);
+        cap = nullptr; dev_seq = nullptr; host = nullptr; host_dev = nullptr; expected = 0;
+    }
+    ~FastState() { clear(); }
+};
+thread_local FastState g_fast;
+
+int fast_init(int dev) {
+    FastState& F = g_fast;
+    if (F.dev == dev && F.host) return QDOT_OK;
+    F.clear();
+    F.dev = dev;
+    QD_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&F.host), PUBLISH_BYTES + 64, cudaHostAllocMapped), "hostalloc");
+    std::memset(F.host, 0, PUBLISH_BYTES + 64);
+    QD_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&F.host_dev), F.host, 0), "mapped ptr");
+    QD_CHECK(cudaMalloc(reinterpret_cast<void**>(&F.dev_seq), sizeof(uint32_t)), "seq");
+    QD_CHECK(cudaMemset(F.dev_seq, 0, sizeof(uint32_t)), "seq");
+    QD_CHECK(cudaStreamCreateWithFlags(&F.cap, cudaStreamNonBlocking), "capture stream");
+    return QDOT_OK;
+}
+
+int enqueue_dot(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                cudaStream_t st) {
+    int r;
+    void* s = static_cast<void*>(st);
+    if ((r = qdot_b200_begin(ws, s))) return r;
+    if ((r = qdot_b200_pass1(x, y, n, norm, cfg, n, ws, s))) return r;
+    if ((r = qdot_b200_score_finalize(ws, n, cfg, s))) return r;
+    if ((r = qdot_b200_pass2(x, y, n, norm, ws, s))) return r;
+    if ((r = qdot_b200_finalize(ws, s))) return r;
+    FastState& F = g_fast;
+    QD_CHECK(launch_publish(static_cast<const char*>(ws) + OFF_RESULT, PUBLISH_BYTES, F.host_dev, F.dev_seq,
+                            reinterpret_cast<uint32_t*>(F.host_dev + PUBLISH_BYTES), st), "publish");
+    return QDOT_OK;
+}
+
+cudaGraphExec_t graph_for(const GraphKey& k, const qdot_config* cfg) {
+    FastState& F = g_fast;
+    for (auto& e : F.cache)
+        if (e.k == k) { e.use = ++F.tick; return e.exec; }
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(F.cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return nullptr;
+    int r = enqueue_dot(k.x, k.y, k.n, k.norm, cfg, k.ws, F.cap);
+    cudaError_t e = cudaStreamEndCapture(F.cap, &g);
+    if (r != QDOT_OK || e != cudaSuccess || !g) { cudaGetLastError(); if (g) cudaGraphDestroy(g); return nullptr; }
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    if ((int)F.cache.size() >= GRAPH_CACHE) {
+        size_t old = 0;
+        for (size_t i = 1; i < F.cache.size(); ++i) if (F.cache[i].use < F.cache[old].use) old = i;
+        cudaGraphExecDestroy(F.cache[old].exec);
+        F.cache.erase(F.cache.begin() + old);
+    }
+    F.cache.push_back({k, exec, ++F.tick});
+    return exec;
+}
+
+// wait for the published block (spinning on the mapped sequence word), then copy out
+int collect(cudaStream_t st, const void* ws, qdot_result* out, qdot_bin* bins, int32_t max_bins) {
+    FastState& F = g_fast;
+    const uint32_t want = ++F.expected;
+    volatile uint32_t* seq = reinterpret_cast<volatile uint32_t*>(F.host + PUBLISH_BYTES);
+    for (uint64_t it = 1; *seq != want; ++it) {
+        if ((it & 1023) == 0) {
+            cudaError_t e = cudaStreamQuery(st);
+            if (e == cudaSuccess && *seq != want) {          // stream idle but nothing published
+                F.expected = *seq;
+                std::snprintf(g_err, sizeof(g_err), "result not published");
+                return QDOT_ERR_CUDA;
+            }
+            if (e != cudaSuccess && e != cudaErrorNotReady) { F.expected = *seq; return cuda_fail(e, "qdot graph"); }
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    std::memcpy(out, F.host, sizeof(qdot_result));
+    const int nb = out->n_bins;
+    const int want_bins = nb < max_bins ? nb : max_bins;
+    const int first = want_bins < FIRST_BINS ? want_bins : FIRST_BINS;
+    if (bins && first > 0) std::memcpy(bins, F.host + 256, sizeof(qdot_bin) * first);
+    if (bins && want_bins > first) {   // rare: many bins -> one more D2H for the rest
+        QD_CHECK(cudaMemcpyAsync(bins + first, static_cast<const char*>(ws) + OFF_BINS + sizeof(qdot_bin) * first,
+                                 sizeof(qdot_bin) * (want_bins - first), cudaMemcpyDeviceToHost, st), "D2H bins");
+        QD_CHECK(cudaStreamSynchronize(st), "sync");
+    }
+    return QDOT_OK;
+}
+
+}  // namespace
+
 int qdot_b200_dot(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
                   qdot_result* out, qdot_bin* bins, int32_t max_bins, void* stream) {
     int v = validate(cfg);
     if (v) return v;
-    int r;
-    if ((r = qdot_b200_begin(ws, stream))) return r;
-    if ((r = qdot_b200_pass1(x, y, n, norm, cfg, n, ws, stream))) return r;
-    if ((r = qdot_b200_score(ws, n, cfg, stream))) return r;
-    if ((r = qdot_b200_pass2(x, y, n, norm, ws, stream))) return r;
-    if ((r = qdot_b200_finalize(ws, stream))) return r;
-    return qdot_b200_fetch(ws, out, bins, max_bins, stream);
+    if (!ws || !out || n < 0 || (n > 0 && (!x || (!norm && !y)))) return QDOT_ERR_ARG;
+    int dev = 0;
+    QD_CHECK(cudaGetDevice(&dev), "cudaGetDevice");
+    if ((v = fast_init(dev))) return v;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    GraphKey k{x, norm ? x : y, n, norm, dev, ws, *cfg};
+    cudaGraphExec_t exec = graph_for(k, cfg);
+    if (exec) {
+        QD_CHECK(cudaGraphLaunch(exec, st), "graph launch");
+    } else if ((v = enqueue_dot(x, norm ? x : y, n, norm, cfg, ws, st))) {   // capture refused: same sequence, eagerly
+        return v;
+    }
+    return collect(st, ws, out, bins, max_bins);
 }
 
 int qdot_b200_dot_host(const double* hx, const double* hy, int64_t n, int norm, const qdot_config* cfg,
@@ -236,7 +379,7 @@ int qdot_b200_dot_host(const double* hx, const double* hy, int64_t n, int norm, 
         cudaStreamWaitEvent(ks, ev, 0);
         if ((rc = qdot_b200_pass1(dx + off, norm ? nullptr : dy + off, len, norm, cfg, n, ws, ks))) goto out_;
     }
-    if ((rc = qdot_b200_score(ws, n, cfg, ks))) goto out_;
+    if ((rc = qdot_b200_score_finalize(ws, n, cfg, ks))) goto out_;
     if ((rc = qdot_b200_pass2(dx, norm ? nullptr : dy, n, norm, ws, ks))) goto out_;
     if ((rc = qdot_b200_finalize(ws, ks))) goto out_;
     rc = qdot_b200_fetch(ws, out, bins, max_bins, ks);

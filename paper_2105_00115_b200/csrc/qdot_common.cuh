@@ -75,6 +75,8 @@ struct ScoreMeta {         // written by the score kernel, read by pass2 / final
     int32_t need_p2;
     int32_t degenerate;
     int32_t input_mu;
+    int32_t done;            // finalize already ran (fused into score: no pass 2 needed)
+    int32_t pad_;
     int64_t nnz;
     int64_t zero;
     int64_t n_total;

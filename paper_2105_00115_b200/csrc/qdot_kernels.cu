@@ -129,10 +129,14 @@ __device__ __forceinline__ long long floor_log2_d(double v, bool* ok) {    // sc
     return flexp_bits(dbits(v));
 }
 
+__device__ void finalize_body(const int64_t* __restrict__ A, const int64_t* __restrict__ B,
+                              const uint32_t* __restrict__ lut_p2, const ScoreMeta& m, qdot_result* __restrict__ res,
+                              qdot_bin* __restrict__ bins);
+
 __global__ void __launch_bounds__(SC_T, 1)
-k_score(const int64_t* __restrict__ A, int32_t* __restrict__ lut_bin, uint32_t* __restrict__ lut_p2,
+k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* __restrict__ lut_bin, uint32_t* __restrict__ lut_p2,
         ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins,
-        int64_t n_total, qdot_config cfg) {
+        int64_t n_total, qdot_config cfg, int fuse) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScShared& S = *reinterpret_cast<ScShared*>(smem_raw);
     const int tid = threadIdx.x;
@@ -320,13 +324,20 @@ k_score(const int64_t* __restrict__ A, int32_t* __restrict__ lut_bin, uint32_t* 
         lut_p2[k] = d;
     }
     need = block_reduce<int>(need, reinterpret_cast<int*>(S.red2), [](int a, int b) { return a | b; }, 0);
+    __shared__ ScoreMeta sm;
     if (tid == 0) {
         ScoreMeta m;
         m.status = S.s_status; m.n_bins = nb; m.e_min = e_min; m.e_max = e_max;
         m.early = early; m.need_p2 = need; m.degenerate = deg; m.input_mu = cfg.input_mu;
+        m.done = (fuse && !need) ? 1 : 0; m.pad_ = 0;
         m.nnz = S.nnz; m.zero = A[A_ZERO]; m.n_total = n_total; m.eps_eff = S.eps_eff;
+        sm = m;
         *meta = m;
     }
+    __syncthreads();
+    // no pass 2 needed (the common case): finalize here and save a launch;
+    // k_finalize then exits on meta->done
+    if (sm.done) finalize_body(A, B, lut_p2, sm, res, bins);
 }
 
 // =============================================================================
@@ -446,23 +457,24 @@ __device__ __forceinline__ double round_i128(__int128 v, int lsb, int mu, int em
 
 constexpr int FN_CHUNK = 1024;
 
-__global__ void __launch_bounds__(FN_T, 1)
-k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const uint32_t* __restrict__ lut_p2,
-           const ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
+// per-bin values + Neumaier fold + result header; any block size (called by
+// k_score with 1024 threads and by k_finalize with FN_T)
+__device__ void finalize_body(const int64_t* __restrict__ A, const int64_t* __restrict__ B,
+                              const uint32_t* __restrict__ lut_p2, const ScoreMeta& m, qdot_result* __restrict__ res,
+                              qdot_bin* __restrict__ bins) {
+    const int nthr = blockDim.x;
     __shared__ double s_val[FN_CHUNK];
-    __shared__ long long s_card[FN_CHUNK];
-    __shared__ signed char s_prec[FN_CHUNK];
     __shared__ int s_ovf, s_half;
     __shared__ double s_s, s_c;
     __shared__ long long s_cnt[4];
     const int tid = threadIdx.x;
-    const ScoreMeta m = *meta;
     if (tid == 0) { s_ovf = 0; s_half = 0; s_s = 0.0; s_c = 0.0; s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0; }
     __syncthreads();
     const int nb = m.status == QDOT_OK ? m.n_bins : 0;
+    long long cnt_local[4] = {0, 0, 0, 0};   // per-thread precision counts (summed after the bins)
     for (int base = 0; base < nb; base += FN_CHUNK) {
         const int cn = nb - base < FN_CHUNK ? nb - base : FN_CHUNK;
-        for (int i = tid; i < cn; i += FN_T) {
+        for (int i = tid; i < cn; i += nthr) {
             const int b = base + i;
             const qdot_bin bn = bins[b];
             const int f = bn.first_key, l = bn.last_key;
@@ -525,26 +537,32 @@ k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const u
             bins[b].value = val;
             bins[b].flags = flags;
             s_val[i] = val;
-            s_card[i] = bn.cardinality;
-            s_prec[i] = (signed char)bn.precision;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) cnt_local[p] += bn.precision == p ? bn.cardinality : 0;
         }
         __syncthreads();
         if (tid == 0) {
             // qdot_accumulate: Neumaier over bins in ascending-upper order (emulate.py:55-72)
             double sum = s_s, c = s_c;
+#pragma unroll 4
             for (int i = 0; i < cn; ++i) {
                 const double v = s_val[i];
                 const double t = __dadd_rn(sum, v);
                 if (fabs(sum) >= fabs(v)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(sum, t), v));
                 else c = __dadd_rn(c, __dadd_rn(__dsub_rn(v, t), sum));
                 sum = t;
-                s_cnt[s_prec[i]] += s_card[i];
             }
             s_s = sum;
             s_c = c;
         }
         __syncthreads();
     }
+    for (int p = 0; p < 4; ++p) {
+        long long v = cnt_local[p];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((tid & 31) == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[p]), (unsigned long long)v);
+    }
+    __syncthreads();
     if (tid == 0) {
         qdot_result r;
         memset(&r, 0, sizeof(r));
@@ -565,6 +583,14 @@ k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const u
         r.half_order_sensitive = s_half;
         *res = r;
     }
+}
+
+__global__ void __launch_bounds__(FN_T, 1)
+k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const uint32_t* __restrict__ lut_p2,
+           const ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
+    const ScoreMeta m = *meta;
+    if (m.done) return;
+    finalize_body(A, B, lut_p2, m, res, bins);
 }
 
 #include "qdot_batched.cuh"
@@ -604,10 +630,10 @@ static int occupancy(K kern, int threads, size_t smem) {
     return occ > 0 ? occ : 1;
 }
 
-template <bool NORM, bool VEC, int V, bool PF, int L2D>
+template <bool NORM, bool VEC, int V, bool PF, int L2D, bool SMALL = false>
 static cudaError_t launch_pass1_t(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
                                   const P1Params& prm, cudaStream_t st) {
-    auto kern = k_pass1<NORM, VEC, V, PF, L2D>;
+    auto kern = k_pass1<NORM, VEC, V, PF, L2D, SMALL>;
     const size_t smem = sizeof(P1Shared);
     static bool attr = false;
     if (!attr) {
@@ -638,6 +664,9 @@ static int p1_variant() {
 template <bool NORM, bool VEC>
 static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
                                   const P1Params& prm, cudaStream_t st) {
+    // short inputs (at most two tiles per SM): the compact variant
+    if ((prm.mode >> 2) == 0 && (prm.mode & 3) == 0 && n <= (int64_t)sm_count_cached() * 2 * (P1_T * 8))
+        return launch_pass1_t<NORM, VEC, 4, false, 0, true>(x, y, n, A, B, prm, st);
     switch (p1_variant()) {
         case 1: return launch_pass1_t<NORM, VEC, 4, false, 0>(x, y, n, A, B, prm, st);   // no L2 prefetch
         case 2: return launch_pass1_t<NORM, VEC, 2, false, 3>(x, y, n, A, B, prm, st);
@@ -657,16 +686,16 @@ cudaError_t launch_pass1(const double* x, const double* y, int64_t n, bool norm,
                : launch_pass1_v<false, false>(x, y, n, A, B, prm, st);
 }
 
-cudaError_t launch_score(const int64_t* A, int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta,
+cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta,
                          qdot_result* res, qdot_bin* bins, int64_t n_total, const qdot_config& cfg,
-                         cudaStream_t st) {
+                         bool fuse, cudaStream_t st) {
     const size_t smem = sizeof(ScShared);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_score<<<1, SC_T, smem, st>>>(A, lut_bin, lut_p2, meta, res, bins, n_total, cfg);
+    k_score<<<1, SC_T, smem, st>>>(A, B, lut_bin, lut_p2, meta, res, bins, n_total, cfg, fuse ? 1 : 0);
     return cudaGetLastError();
 }
 
@@ -703,6 +732,32 @@ cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm,
 cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
                             qdot_result* res, qdot_bin* bins, cudaStream_t st) {
     k_finalize<<<1, FN_T, 0, st>>>(A, B, lut_p2, meta, res, bins);
+    return cudaGetLastError();
+}
+
+// copy the result header and the first `nbins` bins into host-mapped memory,
+// then bump the sequence word the host spins on (written last, after a
+// system-scope fence)
+__global__ void __launch_bounds__(256, 1)
+k_publish(const unsigned char* __restrict__ block, int nbytes, unsigned char* __restrict__ host, uint32_t* dev_seq,
+          volatile uint32_t* host_seq) {
+    const uint4* src = reinterpret_cast<const uint4*>(block);
+    uint4* dst = reinterpret_cast<uint4*>(host);
+    for (int i = threadIdx.x; i < nbytes / 16; i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t sq = *dev_seq + 1;
+        *dev_seq = sq;
+        __threadfence_system();
+        *host_seq = sq;
+    }
+}
+
+cudaError_t launch_publish(const void* block, int nbytes, void* host_dev, uint32_t* dev_seq, uint32_t* host_seq_dev,
+                           cudaStream_t st) {
+    k_publish<<<1, 256, 0, st>>>(static_cast<const unsigned char*>(block), nbytes, static_cast<unsigned char*>(host_dev),
+                                 dev_seq, host_seq_dev);
     return cudaGetLastError();
 }
 

@@ -13,13 +13,15 @@ size_t pass2_smem_bytes();
 
 cudaError_t launch_pass1(const double* x, const double* y, int64_t n, bool norm, int64_t* A, int64_t* B,
                          const P1Params& prm, cudaStream_t st);
-cudaError_t launch_score(const int64_t* A, int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta,
+cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta,
                          qdot_result* res, qdot_bin* bins, int64_t n_total, const qdot_config& cfg,
-                         cudaStream_t st);
+                         bool fuse_finalize, cudaStream_t st);
 cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm, const uint32_t* lut_p2,
                          const ScoreMeta* meta, int64_t* B, cudaStream_t st);
 cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
                             qdot_result* res, qdot_bin* bins, cudaStream_t st);
+cudaError_t launch_publish(const void* block, int nbytes, void* host_dev, uint32_t* dev_seq, uint32_t* host_seq_dev,
+                           cudaStream_t st);
 cudaError_t launch_batched(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, bool norm,
                            const qdot_config& cfg, double* values, int64_t* counts, int32_t* info, cudaStream_t st);
 cudaError_t launch_bin_ids(const double* x, const double* y, int64_t n, bool norm, const int32_t* lut_bin,

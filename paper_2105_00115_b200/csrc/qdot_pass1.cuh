@@ -398,7 +398,10 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
     flush();
 }
 
-template <bool NORM, bool VEC, int V, bool PF, int L2D>
+// SMALL: the variant for short inputs (a few tiles per CTA), where the fixed
+// per-CTA cost dominates: one main loop (full variants, no queue, no L2
+// prefetch) keeps the code a CTA must fetch small.
+template <bool NORM, bool VEC, int V, bool PF, int L2D, bool SMALL>
 __global__ void __launch_bounds__(P1_T, 3)
 k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         int64_t* __restrict__ A, int64_t* __restrict__ B, P1Params prm) {
@@ -492,7 +495,7 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
             S.cbase = cb;
             // lean / full decision (see header); only speed depends on it
             int full = 0;
-            if ((prm.mode & 3) == 2 || prm.input_mu != 52) full = 1;
+            if (SMALL || (prm.mode & 3) == 2 || prm.input_mu != 52) full = 1;
             else if ((prm.mode & 3) == 0) {
                 const uint32_t ns = pref[KEYS];
                 const int fl = flexp_bits(dbits(prm.epsilon));
@@ -523,8 +526,10 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
 
     // ---- main streaming loop (persistent grid over tiles)
     uint32_t zc = 0, nf = 0;
-    const bool fullmode = S.full != 0;
-    if (S.queue) {
+    const bool fullmode = SMALL || S.full != 0;
+    if (SMALL) {
+        p1_main<NORM, VEC, true, false, V, false, 0>(S, x, y, n, A, B, tid, &zc, &nf);
+    } else if (S.queue) {
         if (fullmode) p1_main<NORM, VEC, true, true, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
         else p1_main<NORM, VEC, false, true, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
     } else {
