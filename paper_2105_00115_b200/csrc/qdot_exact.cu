@@ -24,6 +24,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "qdot_common.cuh"
 
 namespace qd {
@@ -55,9 +57,15 @@ constexpr int64_t X_PLAIN_STARTED = X_REGION + 1;
 constexpr int64_t X_RESULT = X_REGION + 8;         // qdot_exact_result (64 bytes)
 constexpr int64_t X_WORDS = X_RESULT + 16;
 
+constexpr int XCW = 128;                // cold window keys (per-CTA limb table)
+
 struct __align__(16) XShared {
     ulonglong2 priv[XW * XT];      // 128-bit signed slot (lo, hi) per (key, thread)
+    // cold window: P = sum l_i 2^(14 i), l_0..l_6 unsigned 14-bit, l_7 signed,
+    // summed with native 32-bit shared atomics (< 2^17 adds between flushes)
+    uint32_t cold[8][XCW];
     int base;
+    int cbase;
 };
 
 __device__ __forceinline__ void split_dbl(uint64_t b, uint64_t& m, int& f) {
@@ -104,24 +112,35 @@ __device__ __noinline__ bool ref_fallback(double x, double y) {
 }
 
 // elements outside the window: zero, non-finite, cold keys, extreme magnitudes
-__device__ __noinline__ void x_cold(int64_t* __restrict__ acc, uint64_t bx, uint64_t by, uint32_t* nf,
-                                    uint32_t* fb) {
-    if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) { (*nf)++; return; }
+// returns 1 for a non-finite element, 2 when the element sends the reference
+// to its Fraction path (see ref_fallback), else 0
+__device__ __noinline__ uint32_t x_cold(XShared& S, int64_t* __restrict__ acc, uint64_t bx, uint64_t by) {
+    if (((bx >> 52) & 0x7FF) == 0x7FF || ((by >> 52) & 0x7FF) == 0x7FF) return 1u;
     uint64_t mx, my;
     int fx, fy;
     split_dbl(bx, mx, fx);
     split_dbl(by, my, fy);
-    if (!mx || !my) return;                                 // zero product contributes nothing
+    if (!mx || !my) return 0u;                              // zero product contributes nothing
+    uint32_t r = 0u;
     // |x| or |y| >= 2^995, or the product near overflow / below 2^-899
     if (fx > 2017 || fy > 2017 || fx + fy > 3066 || fx + fy < 1150)
-        if (ref_fallback(bitsd(bx), bitsd(by))) (*fb)++;
+        if (ref_fallback(bitsd(bx), bitsd(by))) r = 2u;
     uint64_t lo, hi;
     prod128(mx, my, (bx ^ by) >> 63, lo, hi);
-    push_limbs(acc, fx + fy - 2, lo, hi);
+    const int c = fx + fy - 2 - S.cbase;
+    if ((unsigned)c < (unsigned)XCW) {
+        const unsigned __int128 P = ((unsigned __int128)hi << 64) | lo;
+#pragma unroll
+        for (int i = 0; i < 7; ++i) atomicAdd(&S.cold[i][c], (uint32_t)(P >> (14 * i)) & 0x3FFFu);
+        atomicAdd(&S.cold[7][c], (uint32_t)(int32_t)((int64_t)hi >> 34));     // signed top: P >> 98
+    } else {
+        push_limbs(acc, fx + fy - 2, lo, hi);
+    }
+    return r;
 }
 
 __device__ __forceinline__ void x_elem(XShared& S, ulonglong2* __restrict__ my_slots, int base, int64_t* acc,
-                                       double xv, double yv, uint32_t* nf, uint32_t* fb) {
+                                       double xv, double yv, uint32_t& nf, uint32_t& fb) {
     const uint64_t bx = dbits(xv), by = dbits(yv);
     const uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
     const int rel = (int)(fx + fy) - 2 - base;
@@ -137,7 +156,31 @@ __device__ __forceinline__ void x_elem(XShared& S, ulonglong2* __restrict__ my_s
         v.x = nl;
         *slot = v;
     } else {
-        x_cold(acc, bx, by, nf, fb);
+        const uint32_t r = x_cold(S, acc, bx, by);
+        nf += r & 1u;
+        fb += r >> 1;
+    }
+}
+
+struct XTileRegs {
+    double x[2 * XV], y[2 * XV];
+};
+
+template <bool NORM>
+__device__ __forceinline__ void x_load(XTileRegs& T, const double* __restrict__ x, const double* __restrict__ y,
+                                       int64_t t, int tid) {
+    const double2* x2 = reinterpret_cast<const double2*>(x + t * XTILE);
+    const double2* y2 = reinterpret_cast<const double2*>(y + t * XTILE);
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+        const double2 a = __ldcs(x2 + v * XT + tid);
+        T.x[2 * v] = a.x; T.x[2 * v + 1] = a.y;
+        if (!NORM) {
+            const double2 b = __ldcs(y2 + v * XT + tid);
+            T.y[2 * v] = b.x; T.y[2 * v + 1] = b.y;
+        } else {
+            T.y[2 * v] = a.x; T.y[2 * v + 1] = a.y;
+        }
     }
 }
 
@@ -162,10 +205,26 @@ __device__ void x_flush(XShared& S, int64_t* __restrict__ acc, int tid) {
         }
         if (lane == 0 && (lo | hi)) push_limbs(acc, S.base + r, lo, hi);
     }
+    for (int c = tid; c < XCW; c += XT) {
+        unsigned __int128 v = 0;
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < 7; ++i) {
+            const uint32_t l = S.cold[i][c];
+            any |= l != 0;
+            v += (unsigned __int128)l << (14 * i);
+            S.cold[i][c] = 0u;
+        }
+        const int32_t top = (int32_t)S.cold[7][c];
+        any |= top != 0;
+        S.cold[7][c] = 0u;
+        v += (unsigned __int128)((__int128)top * ((__int128)1 << 98));
+        if (any) push_limbs(acc, S.cbase + c, (uint64_t)v, (uint64_t)(v >> 64));
+    }
     __syncthreads();
 }
 
-template <bool NORM>
+template <bool NORM, int PFD>
 __global__ void __launch_bounds__(XT, 3) k_exact(const double* __restrict__ x, const double* __restrict__ y,
                                                  int64_t n, int64_t* __restrict__ acc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -207,10 +266,13 @@ __global__ void __launch_bounds__(XT, 3) k_exact(const double* __restrict__ x, c
             unsigned long long m = 0ull;
             for (int w = 0; w < XT / 32; ++w) m = red[w] > m ? red[w] : m;
             S.base = (m >> 32) ? (int)(0xFFFFFFFFu - (uint32_t)m) : 2046;
+            int cb = S.base - (XCW - XW) / 2;
+            S.cbase = cb < 0 ? 0 : (cb + XCW > XKEYS ? XKEYS - XCW : cb);
         }
     }
     __syncthreads();
     for (int k = tid; k < XW * XT; k += XT) S.priv[k] = make_ulonglong2(0ull, 0ull);
+    for (int k = tid; k < 8 * XCW; k += XT) (&S.cold[0][0])[k] = 0u;
     __syncthreads();
     const int base = S.base;
     ulonglong2* __restrict__ my_slots = S.priv + tid;
@@ -218,36 +280,38 @@ __global__ void __launch_bounds__(XT, 3) k_exact(const double* __restrict__ x, c
     // ---- stream
     uint32_t nf = 0, fb = 0;
     int since = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t e0 = t * XTILE;
-        if (tid == 0 && vec && (t + 3 * (int64_t)gridDim.x + 1) * XTILE <= n) {
-            const int64_t p0 = (t + 3 * (int64_t)gridDim.x) * XTILE;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(x + p0), "r"(XTILE * 8) : "memory");
-            if (!NORM) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(y + p0), "r"(XTILE * 8) : "memory");
-        }
-        double xv[2 * XV], yv[2 * XV];
-        const bool full = vec && e0 + XTILE <= n;
-        if (full) {
-#pragma unroll
-            for (int v = 0; v < XV; ++v) {
-                const double2 a = __ldcs(reinterpret_cast<const double2*>(x + e0) + v * XT + tid);
-                xv[2 * v] = a.x; xv[2 * v + 1] = a.y;
-                if (!NORM) {
-                    const double2 b = __ldcs(reinterpret_cast<const double2*>(y + e0) + v * XT + tid);
-                    yv[2 * v] = b.x; yv[2 * v + 1] = b.y;
-                } else {
-                    yv[2 * v] = a.x; yv[2 * v + 1] = a.y;
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 2 * XV; ++j) x_elem(S, my_slots, base, acc, xv[j], yv[j], &nf, &fb);
-        } else {
-            for (int j = 0; j < 2 * XV; ++j) {
-                const int64_t i = e0 + 2 * ((int64_t)(j >> 1) * XT + tid) + (j & 1);
-                if (i < n) {
-                    const double a = x[i];
-                    x_elem(S, my_slots, base, acc, a, NORM ? a : y[i], &nf, &fb);
-                }
+    const int64_t G = gridDim.x;
+    // full tiles: 128-bit loads of one tile, a bulk L2 prefetch PFD grid-strides ahead
+    const int64_t nfull = vec ? n / XTILE : 0;
+    XTileRegs ta;
+    int64_t t = blockIdx.x;
+    if (t < nfull) x_load<NORM>(ta, x, y, t, tid);
+#define X_PROCESS(T_, t_)                                                                                     \
+    do {                                                                                                      \
+        if (PFD > 0 && tid == 0 && (t_) + PFD * G < nfull) {                                                  \
+            const int64_t p0 = ((t_) + PFD * G) * XTILE;                                                      \
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(x + p0), "r"(XTILE * 8) : "memory"); \
+            if (!NORM)                                                                                        \
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(y + p0), "r"(XTILE * 8) : "memory"); \
+        }                                                                                                     \
+        _Pragma("unroll") for (int j = 0; j < 2 * XV; ++j) x_elem(S, my_slots, base, acc, T_.x[j], T_.y[j], nf, fb); \
+        if (++since == XFLUSH) { x_flush(S, acc, tid); since = 0; }                                           \
+    } while (0)
+    while (t < nfull) {              // single register buffer; the L2 prefetch covers latency
+        if (t != (int64_t)blockIdx.x) x_load<NORM>(ta, x, y, t, tid);
+        X_PROCESS(ta, t);
+        t += G;
+    }
+#undef X_PROCESS
+    // the partial last tile (and every tile of unaligned inputs)
+    for (int64_t t2 = blockIdx.x; t2 < ntiles; t2 += G) {
+        if (t2 < nfull) continue;
+        const int64_t e0 = t2 * XTILE;
+        for (int j = 0; j < 2 * XV; ++j) {
+            const int64_t i = e0 + 2 * ((int64_t)(j >> 1) * XT + tid) + (j & 1);
+            if (i < n) {
+                const double a = x[i];
+                x_elem(S, my_slots, base, acc, a, NORM ? a : y[i], nf, fb);
             }
         }
         if (++since == XFLUSH) { x_flush(S, acc, tid); since = 0; }
@@ -329,9 +393,9 @@ int sm_count() {
     return sms;
 }
 
-template <bool NORM>
-cudaError_t launch_exact(const double* x, const double* y, int64_t n, int64_t* ws, cudaStream_t st) {
-    auto kern = k_exact<NORM>;
+template <bool NORM, int PFD>
+cudaError_t launch_exact_t(const double* x, const double* y, int64_t n, int64_t* ws, cudaStream_t st) {
+    auto kern = k_exact<NORM, PFD>;
     static int occ = 0;
     if (!occ) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(XShared));
@@ -344,6 +408,21 @@ cudaError_t launch_exact(const double* x, const double* y, int64_t n, int64_t* w
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, XT, sizeof(XShared), st>>>(x, y, n, ws);
     return cudaGetLastError();
+}
+
+template <bool NORM>
+cudaError_t launch_exact(const double* x, const double* y, int64_t n, int64_t* ws, cudaStream_t st) {
+    static int var = -1;
+    if (var < 0) {
+        const char* e = getenv("QDOT_B200_X_VARIANT");
+        var = e ? atoi(e) : 0;
+    }
+    switch (var) {
+        case 1: return launch_exact_t<NORM, 0>(x, y, n, ws, st);
+        case 2: return launch_exact_t<NORM, 1>(x, y, n, ws, st);
+        case 3: return launch_exact_t<NORM, 6>(x, y, n, ws, st);
+        default: return launch_exact_t<NORM, 3>(x, y, n, ws, st);
+    }
 }
 
 int fail(cudaError_t e, const char* where) { return qd::report_cuda_error(e, where); }

@@ -14,7 +14,11 @@ y = torch.randn(n, dtype=torch.float64, device=dev, generator=g)
 lib = _lib.load()
 s = stream_handle(dev)
 ws = exact._ExactWs(dev)
-for name, (a, b) in {"c2_normal": (x, y), "wide_exponents": (x * torch.exp2(torch.randint(-300, 300, (n,), device=dev, generator=g).double()), y)}.items():
+from oracle.oracle import gen_illcond
+xi, yi = gen_illcond(n, seed=0)
+cases = {"c2_normal": (x, y), "c3_illcond": (torch.from_numpy(xi).to(dev), torch.from_numpy(yi).to(dev))}
+del xi, yi
+for name, (a, b) in cases.items():
     def run():
         _lib.check(lib.qdot_b200_exact_begin(ws.ptr, s))
         _lib.check(lib.qdot_b200_exact_accumulate(a.data_ptr(), b.data_ptr(), n, 0, ws.ptr, s))
