@@ -64,8 +64,10 @@ struct __align__(16) XShared {
     // cold window: P = sum l_i 2^(14 i), l_0..l_6 unsigned 14-bit, l_7 signed,
     // summed with native 32-bit shared atomics (< 2^17 adds between flushes)
     uint32_t cold[8][XCW];
+    double2 q[XT / 32][32];        // per-warp queue of cold elements (queue mode)
     int base;
     int cbase;
+    int queue;
 };
 
 __device__ __forceinline__ void split_dbl(uint64_t b, uint64_t& m, int& f) {
@@ -139,7 +141,10 @@ __device__ __noinline__ uint32_t x_cold(XShared& S, int64_t* __restrict__ acc, u
     return r;
 }
 
-__device__ __forceinline__ void x_elem(XShared& S, ulonglong2* __restrict__ my_slots, int base, int64_t* acc,
+// QUEUE: elements outside the private window are only flagged (returned
+// true) for the warp queue; otherwise they take x_cold here
+template <bool QUEUE>
+__device__ __forceinline__ bool x_elem(XShared& S, ulonglong2* __restrict__ my_slots, int base, int64_t* acc,
                                        double xv, double yv, uint32_t& nf, uint32_t& fb) {
     const uint64_t bx = dbits(xv), by = dbits(yv);
     const uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
@@ -155,10 +160,37 @@ __device__ __forceinline__ void x_elem(XShared& S, ulonglong2* __restrict__ my_s
         v.y += hi + (nl < lo ? 1 : 0);
         v.x = nl;
         *slot = v;
-    } else {
-        const uint32_t r = x_cold(S, acc, bx, by);
+        return false;
+    }
+    if (QUEUE) return true;
+    const uint32_t r = x_cold(S, acc, bx, by);
+    nf += r & 1u;
+    fb += r >> 1;
+    return false;
+}
+
+// drain the warp's queue, one element per lane (warp-collective)
+__device__ __forceinline__ void x_drain(XShared& S, int64_t* acc, int warp, int lane, uint32_t& qn, uint32_t& nf,
+                                        uint32_t& fb) {
+    __syncwarp();
+    if ((uint32_t)lane < qn) {
+        const double2 e = S.q[warp][lane];
+        const uint32_t r = x_cold(S, acc, dbits(e.x), dbits(e.y));
         nf += r & 1u;
         fb += r >> 1;
+    }
+    qn = 0;
+    __syncwarp();
+}
+
+__device__ __forceinline__ void x_enqueue(XShared& S, int64_t* acc, int warp, int lane, uint32_t& qn, bool c,
+                                          double xv, double yv, uint32_t& nf, uint32_t& fb) {
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    if (m) {
+        const uint32_t k = __popc(m);
+        if (qn + k > 32) x_drain(S, acc, warp, lane, qn, nf, fb);
+        if (c) S.q[warp][qn + __popc(m & ((1u << lane) - 1u))] = make_double2(xv, yv);
+        qn += k;
     }
 }
 
@@ -224,27 +256,80 @@ __device__ void x_flush(XShared& S, int64_t* __restrict__ acc, int tid) {
     __syncthreads();
 }
 
+template <bool NORM, int PFD, bool QUEUE>
+__device__ __forceinline__ void x_stream(XShared& S, const double* __restrict__ x, const double* __restrict__ y,
+                                         int64_t n, int64_t* __restrict__ acc, bool vec, int base, int tid,
+                                         uint32_t& nf, uint32_t& fb) {
+    ulonglong2* __restrict__ my_slots = S.priv + tid;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int64_t ntiles = (n + XTILE - 1) / XTILE;
+    uint32_t qn = 0;                                    // warp queue fill (warp-uniform)
+    int since = 0;
+    const int64_t G = gridDim.x;
+    // full tiles: 128-bit loads of one tile, a bulk L2 prefetch PFD grid-strides ahead
+    const int64_t nfull = vec ? n / XTILE : 0;
+    XTileRegs ta;
+    int64_t t = blockIdx.x;
+    if (t < nfull) x_load<NORM>(ta, x, y, t, tid);
+    while (t < nfull) {
+        if (t != (int64_t)blockIdx.x) x_load<NORM>(ta, x, y, t, tid);
+        if (PFD > 0 && tid == 0 && t + PFD * G < nfull) {
+            const int64_t p0 = (t + PFD * G) * XTILE;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(x + p0), "r"(XTILE * 8) : "memory");
+            if (!NORM) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(y + p0), "r"(XTILE * 8) : "memory");
+        }
+#pragma unroll
+        for (int j = 0; j < 2 * XV; ++j) {
+            const bool c = x_elem<QUEUE>(S, my_slots, base, acc, ta.x[j], ta.y[j], nf, fb);
+            if (QUEUE) x_enqueue(S, acc, warp, lane, qn, c, ta.x[j], ta.y[j], nf, fb);
+        }
+        if (++since == XFLUSH) {
+            if (QUEUE) x_drain(S, acc, warp, lane, qn, nf, fb);
+            x_flush(S, acc, tid);
+            since = 0;
+        }
+        t += G;
+    }
+    // the partial last tile (and every tile of unaligned inputs): direct cold path
+    for (int64_t t2 = blockIdx.x; t2 < ntiles; t2 += G) {
+        if (t2 < nfull) continue;
+        const int64_t e0 = t2 * XTILE;
+        for (int j = 0; j < 2 * XV; ++j) {
+            const int64_t i = e0 + 2 * ((int64_t)(j >> 1) * XT + tid) + (j & 1);
+            if (i < n) {
+                const double a = x[i];
+                x_elem<false>(S, my_slots, base, acc, a, NORM ? a : y[i], nf, fb);
+            }
+        }
+        if (++since == XFLUSH) { x_flush(S, acc, tid); since = 0; }
+    }
+    if (QUEUE) x_drain(S, acc, warp, lane, qn, nf, fb);
+    x_flush(S, acc, tid);
+}
+
 template <bool NORM, int PFD>
 __global__ void __launch_bounds__(XT, 3) k_exact(const double* __restrict__ x, const double* __restrict__ y,
                                                  int64_t n, int64_t* __restrict__ acc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     XShared& S = *reinterpret_cast<XShared*>(smem_raw);
     const int tid = threadIdx.x;
-    const int64_t ntiles = (n + XTILE - 1) / XTILE;
     const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
 
     // ---- window: densest 16 consecutive keys of this CTA's first tile
     uint32_t* hist = reinterpret_cast<uint32_t*>(S.priv);              // XKEYS u32 (reuses the slots)
     for (int k = tid; k < XKEYS; k += XT) hist[k] = 0u;
     __syncthreads();
-    if ((int64_t)blockIdx.x < ntiles) {
-        for (int j = 0; j < 2 * XV; ++j) {
-            const int64_t i = (int64_t)blockIdx.x * XTILE + (int64_t)j * XT + tid;
-            if (i >= n) break;
+    uint32_t nsample = 0;                                            // block-uniform
+    for (int j = 0; j < 2 * XV; ++j) {
+        const int64_t i = (int64_t)blockIdx.x * XTILE + (int64_t)j * XT + tid;
+        bool valid = false;
+        if (i < n) {
             const double a = x[i], b = NORM ? a : y[i];
             const uint32_t fx = (uint32_t)(dbits(a) >> 52) & 0x7FFu, fy = (uint32_t)(dbits(b) >> 52) & 0x7FFu;
-            if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) atomicAdd(&hist[fx + fy - 2], 1u);
+            valid = fx - 1u < 0x7FEu && fy - 1u < 0x7FEu;
+            if (valid) atomicAdd(&hist[fx + fy - 2], 1u);
         }
+        nsample += __syncthreads_count(valid);
     }
     __syncthreads();
     {
@@ -266,6 +351,9 @@ __global__ void __launch_bounds__(XT, 3) k_exact(const double* __restrict__ x, c
             unsigned long long m = 0ull;
             for (int w = 0; w < XT / 32; ++w) m = red[w] > m ? red[w] : m;
             S.base = (m >> 32) ? (int)(0xFFFFFFFFu - (uint32_t)m) : 2046;
+            // queue mode when more than 1/128 of the sample lies outside the private window
+            const uint32_t cov = (uint32_t)(m >> 32);
+            S.queue = (nsample - cov) * 128u > nsample;
             int cb = S.base - (XCW - XW) / 2;
             S.cbase = cb < 0 ? 0 : (cb + XCW > XKEYS ? XKEYS - XCW : cb);
         }
@@ -275,48 +363,11 @@ __global__ void __launch_bounds__(XT, 3) k_exact(const double* __restrict__ x, c
     for (int k = tid; k < 8 * XCW; k += XT) (&S.cold[0][0])[k] = 0u;
     __syncthreads();
     const int base = S.base;
-    ulonglong2* __restrict__ my_slots = S.priv + tid;
 
     // ---- stream
     uint32_t nf = 0, fb = 0;
-    int since = 0;
-    const int64_t G = gridDim.x;
-    // full tiles: 128-bit loads of one tile, a bulk L2 prefetch PFD grid-strides ahead
-    const int64_t nfull = vec ? n / XTILE : 0;
-    XTileRegs ta;
-    int64_t t = blockIdx.x;
-    if (t < nfull) x_load<NORM>(ta, x, y, t, tid);
-#define X_PROCESS(T_, t_)                                                                                     \
-    do {                                                                                                      \
-        if (PFD > 0 && tid == 0 && (t_) + PFD * G < nfull) {                                                  \
-            const int64_t p0 = ((t_) + PFD * G) * XTILE;                                                      \
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(x + p0), "r"(XTILE * 8) : "memory"); \
-            if (!NORM)                                                                                        \
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(y + p0), "r"(XTILE * 8) : "memory"); \
-        }                                                                                                     \
-        _Pragma("unroll") for (int j = 0; j < 2 * XV; ++j) x_elem(S, my_slots, base, acc, T_.x[j], T_.y[j], nf, fb); \
-        if (++since == XFLUSH) { x_flush(S, acc, tid); since = 0; }                                           \
-    } while (0)
-    while (t < nfull) {              // single register buffer; the L2 prefetch covers latency
-        if (t != (int64_t)blockIdx.x) x_load<NORM>(ta, x, y, t, tid);
-        X_PROCESS(ta, t);
-        t += G;
-    }
-#undef X_PROCESS
-    // the partial last tile (and every tile of unaligned inputs)
-    for (int64_t t2 = blockIdx.x; t2 < ntiles; t2 += G) {
-        if (t2 < nfull) continue;
-        const int64_t e0 = t2 * XTILE;
-        for (int j = 0; j < 2 * XV; ++j) {
-            const int64_t i = e0 + 2 * ((int64_t)(j >> 1) * XT + tid) + (j & 1);
-            if (i < n) {
-                const double a = x[i];
-                x_elem(S, my_slots, base, acc, a, NORM ? a : y[i], nf, fb);
-            }
-        }
-        if (++since == XFLUSH) { x_flush(S, acc, tid); since = 0; }
-    }
-    x_flush(S, acc, tid);
+    if (S.queue) x_stream<NORM, PFD, true>(S, x, y, n, acc, vec, base, tid, nf, fb);
+    else x_stream<NORM, PFD, false>(S, x, y, n, acc, vec, base, tid, nf, fb);
     unsigned long long a = nf, b = fb;
     for (int o = 16; o; o >>= 1) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
