@@ -14,7 +14,9 @@ allreduce(A) + score + pass2 + allreduce(B) + finalize.
 
 `value` = elements/s with inputs resident in HBM (CUDA events, max over
 ranks); `e2e` = the same metric through the public API qdot() from pinned
-host memory (H2D of x, y and the D2H of the result inside the timed region).
+host memory (H2D of x, y and the D2H of the result inside the timed region;
+qdot() streams host inputs in 64 MiB chunks, the copy of chunk k+1
+overlapping pass 1 on chunk k, so e2e runs at the PCIe H2D rate).
 Inputs (4 GiB per GPU) are far larger than the 126 MB L2, so no L2 flush is
 needed between steps.
 

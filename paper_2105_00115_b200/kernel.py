@@ -227,15 +227,97 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
         half_order_sensitive=bool(res.half_order_sensitive))
 
 
+# host inputs at least this long are streamed to the device in chunks that
+# pass 1 consumes while the next chunk is in flight (copy / compute overlap)
+PIPELINE_MIN = 1 << 22
+PIPELINE_CHUNK = 1 << 23
+
+
+def _host_vector(a):
+    """1-D float64 contiguous CPU torch tensor for a host input, or None when `a`
+    is already on a CUDA device."""
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            return None
+        t = a
+        if t.dim() != 1:
+            raise ValueError("inputs must be 1-D arrays")
+        return t.to(torch.float64).contiguous()
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    if arr.ndim != 1:
+        raise ValueError("inputs must be 1-D arrays")
+    return torch.from_numpy(arr)
+
+
+def _run_host_pipelined(xh, yh, norm: bool, cfg: ToleranceConfig, strategy):
+    """H2D of chunk k+1 (copy stream) overlaps pass 1 on chunk k (compute
+    stream); then score / pass 2 / finalize on the resident vectors.
+    Returns (result, bins, phase_ns, xd, yd)."""
+    import torch
+    device = torch.device("cuda", torch.cuda.current_device())
+    n = int(xh.shape[0])
+    lib = _lib.load()
+    st = thread_state(device)
+    c = config_struct(cfg, strategy)
+    comp = torch.cuda.current_stream(device)
+    copy = getattr(st, "copy_stream", None)
+    if copy is None:
+        copy = st.copy_stream = torch.cuda.Stream(device)
+    s = comp.cuda_stream
+    xd = torch.empty(n, dtype=torch.float64, device=device)
+    yd = xd if norm else torch.empty(n, dtype=torch.float64, device=device)
+    xd.record_stream(copy)
+    yd.record_stream(copy)
+    ws = st.ws_ptr
+    st.ev[0].record(comp)
+    _lib.check(lib.qdot_b200_begin(ws, s), lib)
+    copy.wait_stream(comp)                      # the buffers are free to overwrite
+    for off in range(0, n, PIPELINE_CHUNK):
+        ln = min(PIPELINE_CHUNK, n - off)
+        with torch.cuda.stream(copy):
+            xd[off:off + ln].copy_(xh[off:off + ln], non_blocking=True)
+            if not norm:
+                yd[off:off + ln].copy_(yh[off:off + ln], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        comp.wait_event(ev)
+        _lib.check(lib.qdot_b200_pass1(xd.data_ptr() + 8 * off, yd.data_ptr() + 8 * off, ln, int(norm),
+                                       ctypes.byref(c), n, ws, s), lib)
+    _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), s), lib)
+    st.ev[1].record(comp)
+    _lib.check(lib.qdot_b200_pass2(xd.data_ptr(), yd.data_ptr(), n, int(norm), ws, s), lib)
+    _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+    st.ev[2].record(comp)
+    _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
+    phase = {"select": int(st.ev[0].elapsed_time(st.ev[1]) * 1e6),
+             "compute": int(st.ev[1].elapsed_time(st.ev[2]) * 1e6), "reference": 0}
+    return st.result, st.bins, phase, xd, yd
+
+
 def qdot(x, y, cfg: ToleranceConfig, strategy: Strategy = None, reference=None) -> QdotReport:
     """Approximate dot product with audit report (kernel.py:179-240).
 
     x, y: array-likes (coerced like np.ascontiguousarray(float64) and copied
     to the current CUDA device) or CUDA/CPU torch tensors (float64 CUDA
     tensors are used in place).  ``x is y`` selects norm mode (one read).
+    Long host inputs are streamed in chunks with the copy overlapping pass 1.
     """
     if strategy is None:
         strategy = ExactBinning()
+    require_cuda()
+    is_norm = x is y                                           # kernel.py:194
+    xh = _host_vector(x)
+    if xh is not None and xh.shape[0] >= PIPELINE_MIN:
+        yh = xh if is_norm else _host_vector(y)
+        if yh is not None:
+            if xh.shape[0] != yh.shape[0]:                     # floatbits.py:68-69
+                raise ValueError(f"length mismatch: {xh.shape[0]} vs {yh.shape[0]}")
+            n = int(xh.shape[0])
+            res, cbins, phase, xd, yd = _run_host_pipelined(xh, yh, is_norm, cfg, strategy)
+            _raise_status(res)
+            indexer = _Indexer(xd, yd, n, is_norm, xd.device)
+            return report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer)
     is_norm, xd, yd = _prepare(x, y)
     n = int(xd.shape[0])
     res, cbins, phase = run_device(xd, yd, n, is_norm, cfg, strategy)

@@ -279,3 +279,25 @@ def test_qdot_sharded_single_rank_nccl():
             [(u.lower, u.upper, u.cardinality) for u in b.params.bins]
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("norm", [False, True])
+def test_host_inputs_pipelined_equal_device(norm):
+    # host inputs above PIPELINE_MIN stream in chunks overlapping pass 1; the
+    # report must equal the one for the same vectors already on the device
+    from paper_2105_00115_b200 import kernel
+    rng = np.random.default_rng(77)
+    n = kernel.PIPELINE_MIN + 3 * kernel.PIPELINE_CHUNK // 2 + 12345
+    x = rng.standard_normal(n) * np.exp2(rng.integers(-30, 30, n))
+    y = x if norm else rng.standard_normal(n)
+    cfg = Q.ToleranceConfig(1e-9, Q.SplitMode.PER_BIN)
+    for strategy in (Q.ExactBinning(), Q.RangedBinning(3)):
+        a = Q.qdot(x, y, cfg, strategy=strategy)                              # numpy (pageable)
+        xt = torch.from_numpy(x).pin_memory()
+        b = Q.qdot(xt, xt if norm else torch.from_numpy(y).pin_memory(), cfg, strategy=strategy)   # pinned
+        xd = torch.from_numpy(x).cuda()
+        d = Q.qdot(xd, xd if norm else torch.from_numpy(y).cuda(), cfg, strategy=strategy)        # device
+        for r in (a, b):
+            assert r.value == d.value and r.counts == d.counts and r.abs_bound == d.abs_bound
+            assert [(q.lower, q.upper, q.cardinality, q.precision) for q in r.params.bins] == \
+                   [(q.lower, q.upper, q.cardinality, q.precision) for q in d.params.bins]
