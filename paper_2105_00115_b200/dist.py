@@ -76,11 +76,18 @@ def qdot_sharded(x_local, y_local, cfg: ToleranceConfig, strategy: Strategy = No
         strategy = ExactBinning()
     is_norm = x_local is y_local
     device = torch.device("cuda", torch.cuda.current_device())
-    xd, _ = as_device_vector(x_local, device)
-    yd = xd if is_norm else as_device_vector(y_local, device)[0]
-    if xd.shape[0] != yd.shape[0]:
-        raise ValueError(f"length mismatch: {xd.shape[0]} vs {yd.shape[0]}")
-    n = int(xd.shape[0])
+    from .kernel import PIPELINE_MIN, _host_vector, h2d_pass1
+    xh = _host_vector(x_local)
+    yh = None if xh is None else (xh if is_norm else _host_vector(y_local))
+    if xh is not None and yh is not None and xh.shape[0] != yh.shape[0]:
+        raise ValueError(f"length mismatch: {xh.shape[0]} vs {yh.shape[0]}")
+    streamed = xh is not None and yh is not None and xh.shape[0] >= PIPELINE_MIN
+    if not streamed:
+        xd, _ = as_device_vector(x_local, device)
+        yd = xd if is_norm else as_device_vector(y_local, device)[0]
+        if xd.shape[0] != yd.shape[0]:
+            raise ValueError(f"length mismatch: {xd.shape[0]} vs {yd.shape[0]}")
+    n = int(xh.shape[0]) if streamed else int(xd.shape[0])
     if n_total is None:
         t = torch.tensor([n], dtype=torch.int64, device=device)
         dist.all_reduce(t, group=group)
@@ -90,10 +97,13 @@ def qdot_sharded(x_local, y_local, cfg: ToleranceConfig, strategy: Strategy = No
     c = config_struct(cfg, strategy)
     s = stream_handle(device)
     ws = st.ws_ptr
+    _lib.check(lib.qdot_b200_begin(ws, s), lib)
+    if streamed:        # host shard: H2D in chunks overlapping pass 1
+        xd, yd = h2d_pass1(xh, yh, is_norm, c, n_total, st, device)
     xp = xd.data_ptr()
     yp = xp if is_norm else yd.data_ptr()
-    _lib.check(lib.qdot_b200_begin(ws, s), lib)
-    _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(is_norm), ctypes.byref(c), n_total, ws, s), lib)
+    if not streamed:
+        _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(is_norm), ctypes.byref(c), n_total, ws, s), lib)
     reduce_regions(st.region_a(), None, group)
     _lib.check(lib.qdot_b200_score(ws, n_total, ctypes.byref(c), s), lib)
     _lib.check(lib.qdot_b200_pass2(xp, yp, n, int(is_norm), ws, s), lib)

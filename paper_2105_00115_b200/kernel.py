@@ -250,16 +250,13 @@ def _host_vector(a):
     return torch.from_numpy(arr)
 
 
-def _run_host_pipelined(xh, yh, norm: bool, cfg: ToleranceConfig, strategy):
-    """H2D of chunk k+1 (copy stream) overlaps pass 1 on chunk k (compute
-    stream); then score / pass 2 / finalize on the resident vectors.
-    Returns (result, bins, phase_ns, xd, yd)."""
+def h2d_pass1(xh, yh, norm: bool, c, n_total: int, st, device):
+    """Copy host vectors to new device buffers in PIPELINE_CHUNK pieces on a
+    copy stream while pass 1 (current stream, workspace already begun)
+    consumes each piece as it lands.  Returns the device vectors."""
     import torch
-    device = torch.device("cuda", torch.cuda.current_device())
     n = int(xh.shape[0])
     lib = _lib.load()
-    st = thread_state(device)
-    c = config_struct(cfg, strategy)
     comp = torch.cuda.current_stream(device)
     copy = getattr(st, "copy_stream", None)
     if copy is None:
@@ -269,9 +266,6 @@ def _run_host_pipelined(xh, yh, norm: bool, cfg: ToleranceConfig, strategy):
     yd = xd if norm else torch.empty(n, dtype=torch.float64, device=device)
     xd.record_stream(copy)
     yd.record_stream(copy)
-    ws = st.ws_ptr
-    st.ev[0].record(comp)
-    _lib.check(lib.qdot_b200_begin(ws, s), lib)
     copy.wait_stream(comp)                      # the buffers are free to overwrite
     for off in range(0, n, PIPELINE_CHUNK):
         ln = min(PIPELINE_CHUNK, n - off)
@@ -283,7 +277,26 @@ def _run_host_pipelined(xh, yh, norm: bool, cfg: ToleranceConfig, strategy):
             ev.record(copy)
         comp.wait_event(ev)
         _lib.check(lib.qdot_b200_pass1(xd.data_ptr() + 8 * off, yd.data_ptr() + 8 * off, ln, int(norm),
-                                       ctypes.byref(c), n, ws, s), lib)
+                                       ctypes.byref(c), n_total, st.ws_ptr, s), lib)
+    return xd, yd
+
+
+def _run_host_pipelined(xh, yh, norm: bool, cfg: ToleranceConfig, strategy):
+    """H2D of chunk k+1 (copy stream) overlaps pass 1 on chunk k (compute
+    stream); then score / pass 2 / finalize on the resident vectors.
+    Returns (result, bins, phase_ns, xd, yd)."""
+    import torch
+    device = torch.device("cuda", torch.cuda.current_device())
+    n = int(xh.shape[0])
+    lib = _lib.load()
+    st = thread_state(device)
+    c = config_struct(cfg, strategy)
+    comp = torch.cuda.current_stream(device)
+    s = comp.cuda_stream
+    ws = st.ws_ptr
+    st.ev[0].record(comp)
+    _lib.check(lib.qdot_b200_begin(ws, s), lib)
+    xd, yd = h2d_pass1(xh, yh, norm, c, n, st, device)
     _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), s), lib)
     st.ev[1].record(comp)
     _lib.check(lib.qdot_b200_pass2(xd.data_ptr(), yd.data_ptr(), n, int(norm), ws, s), lib)

@@ -277,6 +277,12 @@ def test_qdot_sharded_single_rank_nccl():
         assert a.value == b.value and a.counts == b.counts and a.abs_bound == b.abs_bound
         assert [(u.lower, u.upper, u.cardinality) for u in a.params.bins] == \
             [(u.lower, u.upper, u.cardinality) for u in b.params.bins]
+        # a host shard above PIPELINE_MIN takes the chunked H2D / pass-1 overlap path
+        from paper_2105_00115_b200 import kernel
+        xl, yl = O.gen_illcond(kernel.PIPELINE_MIN + 4097, seed=5)
+        c = qdot_sharded(torch.from_numpy(xl).pin_memory(), torch.from_numpy(yl).pin_memory(), cfg)
+        d = Q.qdot(torch.from_numpy(xl).cuda(), torch.from_numpy(yl).cuda(), cfg)
+        assert c.value == d.value and c.counts == d.counts and c.abs_bound == d.abs_bound
     finally:
         dist.destroy_process_group()
 
