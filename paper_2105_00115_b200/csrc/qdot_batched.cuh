@@ -150,11 +150,8 @@ __device__ __forceinline__ void b_elems(BWarp& W, ulonglong2* __restrict__ my, i
             const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv[j], yv[j]), scale));
             const uint64_t bx = dbits(xv[j]), by = dbits(yv[j]);
             int32_t ks, kh;
-            exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
-                           bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
-            const int32_t s32 = (int32_t)(hx ^ hy) >> 31;
-            ks = (ks ^ s32) - s32;
-            kh = (kh ^ s32) - s32;
+            exact_variants_signed(bitsd((bx & 0x800FFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
+                                  bitsd((by & 0x800FFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
             ulonglong2* slot = my + rel * 32;
             ulonglong2 v = *slot;
             v.x += (unsigned long long)kd;

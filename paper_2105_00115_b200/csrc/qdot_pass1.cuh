@@ -82,6 +82,17 @@ __device__ __forceinline__ void exact_variants(double mx, double my, int32_t& ks
     kh = (int32_t)(((hb & 0x3FFu) | 0x400u) << ((hb >> 10) - 15));        // units of 2^-10
 }
 
+// the same from SIGNED mantissas (|mx|, |my| in [1,2), signs of x and y): the
+// format products carry the sign (RNE is sign-symmetric) and one scaled
+// float->int conversion yields the signed units -- no bit extraction, no
+// separate sign fix
+__device__ __forceinline__ void exact_variants_signed(double sx, double sy, int32_t& ks, int32_t& kh) {
+    const float ps = __fmul_rn(__double2float_rn(sx), __double2float_rn(sy));          // |ps| in [1, 4]
+    ks = __float2int_rn(__fmul_rn(ps, 8388608.0f));                                    // exact: units of 2^-23
+    const float ph = __half2float(__hmul(__double2half(sx), __double2half(sy)));       // exact widening
+    kh = __float2int_rn(__fmul_rn(ph, 1024.0f));                                       // units of 2^-10
+}
+
 // cold key: variants from the mantissa bits (mbx, mby = raw bits of mx, my),
 // then the per-CTA limb table or, outside it, global atomics
 __device__ __forceinline__ void p1_cold(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B, int key,
@@ -148,11 +159,8 @@ __device__ __forceinline__ bool p1_elem(P1Shared& S, ulonglong2* __restrict__ my
         if (FULL) {
             const uint64_t bx = dbits(xv), by = dbits(yv);
             int32_t ks, kh;
-            exact_variants(bitsd((bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
-                           bitsd((by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
-            const int32_t s32 = (int32_t)(hx ^ hy) >> 31;
-            ks = (ks ^ s32) - s32;
-            kh = (kh ^ s32) - s32;
+            exact_variants_signed(bitsd((bx & 0x800FFFFFFFFFFFFFull) | 0x3FF0000000000000ull),
+                                  bitsd((by & 0x800FFFFFFFFFFFFFull) | 0x3FF0000000000000ull), ks, kh);
             v.y += (unsigned long long)(((long long)ks << 29) + ((long long)kh << 8) + 1);
         } else {
             v.y = (unsigned long long)((uint32_t)v.y + 1u);   // count < 2^32 between flushes
