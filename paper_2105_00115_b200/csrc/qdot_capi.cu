@@ -113,7 +113,7 @@ int qdot_b200_begin(void* ws, void* stream) {
     if (!ws) return QDOT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // regions A and B are contiguous
-    QD_CHECK(cudaMemsetAsync(static_cast<char*>(ws) + OFF_A, 0, (size_t)(BYTES_A + BYTES_B), st), "memset");
+    QD_CHECK(cudaMemsetAsync(static_cast<char*>(ws) + OFF_A, 0, (size_t)(BYTES_A + BYTES_B + BYTES_LOCAL), st), "memset");
     return QDOT_OK;
 }
 
@@ -125,11 +125,18 @@ int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const
     prm.input_mu = 52;
     prm.mode = 1;   // no config: lean
     prm.n_total = n_total > n ? n_total : n;
+    {
+        WsPtrs w0 = ws_ptrs(ws);
+        prm.list = w0.list;
+        prm.list_fill = w0.list_fill;
+        prm.collect = 0;
+    }
     if (cfg) {
         int v = validate(cfg);
         if (v) return v;
         prm.epsilon = cfg->epsilon;
         prm.input_mu = cfg->input_mu;
+        prm.collect = cfg->strategy != QDOT_STRATEGY_EXACT;
         prm.mode = cfg->reserved;   // bits 0-1: 0 auto, 1 lean, 2 full; bits 2-3: queue 0 auto, 4 on, 8 off
         if (prm.mode < 0 || (prm.mode & 3) > 2 || (prm.mode >> 2) > 2) return QDOT_ERR_ARG;
     }
@@ -159,7 +166,8 @@ int qdot_b200_score_finalize(void* ws, int64_t n_total, const qdot_config* cfg, 
 int qdot_b200_pass2(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream) {
     if (!ws || n < 0 || (n > 0 && (!x || (!norm && !y)))) return QDOT_ERR_ARG;
     WsPtrs w = ws_ptrs(ws);
-    QD_CHECK(launch_pass2(x, norm ? x : y, n, norm != 0, w.lut_p2, w.meta, w.b, static_cast<cudaStream_t>(stream)),
+    QD_CHECK(launch_pass2(x, norm ? x : y, n, norm != 0, w.lut_p2, w.meta, w.b, w.list, w.list_fill,
+                          static_cast<cudaStream_t>(stream)),
              "pass2");
     return QDOT_OK;
 }

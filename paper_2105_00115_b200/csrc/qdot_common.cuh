@@ -38,9 +38,12 @@ constexpr int64_t A_ZERO = KEYS;        // zero-product count
 constexpr int64_t A_NONFINITE = KEYS + 1;
 constexpr int64_t A_FULLCTAS = KEYS + 2;  // pass-1 CTAs that ran the full-variant loop (diagnostic)
 constexpr int64_t A_LEANCTAS = KEYS + 3;  // pass-1 CTAs that ran the lean loop (diagnostic)
+constexpr int64_t A_LISTOVF = KEYS + 4;   // ranks whose cold-element list overflowed
 constexpr int64_t A_HOT = 4224;         // [KEYS]: elements of the key accumulated by a lean
                                         // private window (exact HALF/SINGLE variants absent)
-constexpr int64_t A_LEN = 8448;         // padded
+constexpr int64_t A_PRIV = 8448;        // [KEYS]: elements of the key accumulated by any private
+                                        // window (absent from the cold-element list)
+constexpr int64_t A_LEN = 12672;        // padded
 
 constexpr int64_t B_D0 = 0;             // DOUBLE limbs, weights 2^0, 2^32, 2^64, 2^96
 constexpr int64_t B_D1 = 1 * (int64_t)KEYS;
@@ -65,6 +68,9 @@ struct P1Params {
     int64_t n_total;
     int32_t input_mu;
     int32_t mode;            // 0 auto, 1 force lean, 2 force full variants
+    double2* list;           // cold-element list: LIST_SLOTS slots of LIST_PER_SLOT entries,
+    uint32_t* list_fill;     // slot b filled by pass-1 CTA b (fill kept across launches)
+    int32_t collect;         // fill the list (ranged / split strategies: pass 2 may need it)
 };
 
 struct ScoreMeta {         // written by the score kernel, read by pass2 / finalize
@@ -87,13 +93,22 @@ constexpr int64_t BYTES_A = A_LEN * 8;
 constexpr int64_t BYTES_B = B_LEN * 8;
 constexpr int64_t OFF_A = 0;
 constexpr int64_t OFF_B = OFF_A + BYTES_A;
-constexpr int64_t OFF_LUT_BIN = OFF_B + BYTES_B;                 // int32[KEYS]
+constexpr int64_t OFF_LOCAL = OFF_B + BYTES_B;                   // rank-local counters (zeroed by begin)
+constexpr int64_t LIST_SLOTS = 1024;                             // one list slot per pass-1 CTA index
+constexpr int64_t BYTES_LOCAL = LIST_SLOTS * 4;                  // uint32 fill per slot
+constexpr int64_t OFF_LUT_BIN = OFF_LOCAL + BYTES_LOCAL;         // int32[KEYS]
 constexpr int64_t OFF_LUT_P2 = OFF_LUT_BIN + 4224 * 4;           // uint32[KEYS]
 constexpr int64_t OFF_META = OFF_LUT_P2 + 4224 * 4;              // ScoreMeta
 constexpr int64_t OFF_RESULT = OFF_META + 256;                   // qdot_result
 constexpr int64_t OFF_BINS = OFF_RESULT + 256;                   // qdot_bin[KEYS + 1]
 constexpr int64_t BYTES_BINS = (int64_t)sizeof(qdot_bin) * (KEYS + 1);
-constexpr int64_t WS_BYTES = ((OFF_BINS + BYTES_BINS + 255) / 256) * 256;
+// cold-element list: (x, y) of every element pass 1 did not accumulate in a
+// private window, so that pass 2 (when it is needed only for such keys) reads
+// this list instead of streaming both vectors again
+constexpr int64_t LIST_CAP = 1 << 22;                             // entries (64 MiB)
+constexpr int64_t LIST_PER_SLOT = LIST_CAP / LIST_SLOTS;
+constexpr int64_t OFF_LIST = ((OFF_BINS + BYTES_BINS + 255) / 256) * 256;
+constexpr int64_t WS_BYTES = OFF_LIST + LIST_CAP * 16;
 
 static_assert(sizeof(ScoreMeta) <= 256, "meta");
 static_assert(sizeof(qdot_result) <= 256, "result");
@@ -102,6 +117,8 @@ static_assert(sizeof(qdot_bin) == 56, "bin layout");
 struct WsPtrs {
     int64_t* a;
     int64_t* b;
+    uint32_t* list_fill;              // OFF_LOCAL: fill of each CTA slot
+    double2* list;
     int32_t* lut_bin;
     uint32_t* lut_p2;
     ScoreMeta* meta;
@@ -114,6 +131,8 @@ inline WsPtrs ws_ptrs(void* ws) {
     WsPtrs w;
     w.a = reinterpret_cast<int64_t*>(p + OFF_A);
     w.b = reinterpret_cast<int64_t*>(p + OFF_B);
+    w.list_fill = reinterpret_cast<uint32_t*>(p + OFF_LOCAL);
+    w.list = reinterpret_cast<double2*>(p + OFF_LIST);
     w.lut_bin = reinterpret_cast<int32_t*>(p + OFF_LUT_BIN);
     w.lut_p2 = reinterpret_cast<uint32_t*>(p + OFF_LUT_P2);
     w.meta = reinterpret_cast<ScoreMeta*>(p + OFF_META);

@@ -305,8 +305,9 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
     }
     __syncthreads();
     __threadfence_block();
-    // ---- LUTs
-    int need = 0;
+    // ---- LUTs.  need: some key needs pass 2; priv: such a key also has
+    // elements accumulated in private windows (not in the cold-element list)
+    int need = 0, priv = 0;
     for (int k = tid; k < KEYS; k += SC_T) {
         int b = S.bin_of[k];
         lut_bin[k] = b;
@@ -319,11 +320,16 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
                 d = P2_NEED | (pr == QDOT_HALF ? P2_HALF : 0u) |
                     (uint32_t)(delta > P2_DELTA_MAX ? P2_DELTA_MAX : delta);
                 need = 1;
+                if (A[A_PRIV + k] > 0) priv = 1;
             }
         }
         lut_p2[k] = d;
     }
     need = block_reduce<int>(need, reinterpret_cast<int*>(S.red2), [](int a, int b) { return a | b; }, 0);
+    priv = block_reduce<int>(priv, reinterpret_cast<int*>(S.red2), [](int a, int b) { return a | b; }, 0);
+    // pass 2 mode: 2 = only over the cold-element list (every element of every
+    // pass-2 key is in it, no slot overflowed), 1 = stream x and y again
+    if (need) need = (!priv && A[A_LISTOVF] == 0) ? 2 : 1;
     __shared__ ScoreMeta sm;
     if (tid == 0) {
         ScoreMeta m;
@@ -378,16 +384,44 @@ __device__ __forceinline__ long long scaled_units(double mx, double my, uint32_t
     }
 }
 
+// one element of pass 2 (zeros and tail padding contribute nothing)
+__device__ __forceinline__ void p2_elem(P2Shared& S, double a, double b) {
+    if (a == 0.0 || b == 0.0) return;
+    const uint64_t bx = dbits(a), by = dbits(b);
+    const int e = flexp_bits(bx) + flexp_bits(by);
+    const uint32_t info = S.lut[e + KOFF];
+    if (!(info & P2_NEED)) return;
+    long long k = scaled_units(bitsd(mant_bits(bx)), bitsd(mant_bits(by)), info);
+    if ((bx ^ by) >> 63) k = -k;
+    atomicAdd(&S.acc[e + KOFF], (unsigned long long)k);
+}
+
 template <bool NORM, bool VEC>
 __global__ void __launch_bounds__(P2_T)
 k_pass2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-        const uint32_t* __restrict__ lut_p2, const ScoreMeta* __restrict__ meta, int64_t* __restrict__ B) {
-    if (!meta->need_p2 || meta->status != QDOT_OK) return;
+        const uint32_t* __restrict__ lut_p2, const ScoreMeta* __restrict__ meta, int64_t* __restrict__ B,
+        const double2* __restrict__ list, const uint32_t* __restrict__ list_fill) {
+    const int mode = meta->need_p2;
+    if (!mode || meta->status != QDOT_OK) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     P2Shared& S = *reinterpret_cast<P2Shared*>(smem_raw);
     const int tid = threadIdx.x;
     for (int k = tid; k < KEYS; k += P2_T) { S.acc[k] = 0ull; S.lut[k] = lut_p2[k]; }
     __syncthreads();
+    if (mode == 2) {
+        // only the cold-element list: slot s holds list_fill[s] entries
+        for (int sl = blockIdx.x; sl < (int)LIST_SLOTS; sl += gridDim.x) {
+            const uint32_t cnt = min(list_fill[sl], (uint32_t)LIST_PER_SLOT);
+            for (uint32_t i = tid; i < cnt; i += P2_T) {
+                const double2 e = list[(int64_t)sl * LIST_PER_SLOT + i];
+                p2_elem(S, e.x, e.y);
+            }
+        }
+        __syncthreads();
+        for (int k = tid; k < KEYS; k += P2_T)
+            if (S.acc[k]) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_P2 + k), S.acc[k]);
+        return;
+    }
     const int64_t ntiles = (n + P2_TILE - 1) / P2_TILE;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         double xv[2 * P2_V], yv[2 * P2_V];
@@ -412,17 +446,7 @@ k_pass2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
             }
         }
 #pragma unroll
-        for (int j = 0; j < 2 * P2_V; ++j) {
-            double a = xv[j], b = NORM ? xv[j] : yv[j];
-            if (a == 0.0 || b == 0.0) continue;   // zeros and tail padding
-            uint64_t bx = dbits(a), by = dbits(b);
-            int e = flexp_bits(bx) + flexp_bits(by);
-            uint32_t info = S.lut[e + KOFF];
-            if (!(info & P2_NEED)) continue;
-            long long k = scaled_units(bitsd(mant_bits(bx)), bitsd(mant_bits(by)), info);
-            if ((bx ^ by) >> 63) k = -k;
-            atomicAdd(&S.acc[e + KOFF], (unsigned long long)k);
-        }
+        for (int j = 0; j < 2 * P2_V; ++j) p2_elem(S, xv[j], NORM ? xv[j] : yv[j]);
     }
     __syncthreads();
     for (int k = tid; k < KEYS; k += P2_T)
@@ -701,7 +725,8 @@ cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, u
 
 template <bool NORM, bool VEC>
 static cudaError_t launch_pass2_t(const double* x, const double* y, int64_t n, const uint32_t* lut_p2,
-                                  const ScoreMeta* meta, int64_t* B, cudaStream_t st) {
+                                  const ScoreMeta* meta, int64_t* B, const double2* list, const uint32_t* list_fill,
+                                  cudaStream_t st) {
     auto kern = k_pass2<NORM, VEC>;
     const size_t smem = sizeof(P2Shared);
     static bool attr = false;
@@ -715,18 +740,19 @@ static cudaError_t launch_pass2_t(const double* x, const double* y, int64_t n, c
     int64_t grid = (int64_t)sm_count_cached() * occ;
     if (grid > ntiles) grid = ntiles;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, P2_T, smem, st>>>(x, y, n, lut_p2, meta, B);
+    kern<<<(unsigned)grid, P2_T, smem, st>>>(x, y, n, lut_p2, meta, B, list, list_fill);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm, const uint32_t* lut_p2,
-                         const ScoreMeta* meta, int64_t* B, cudaStream_t st) {
+                         const ScoreMeta* meta, int64_t* B, const double2* list, const uint32_t* list_fill,
+                         cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     bool vec = ((reinterpret_cast<uintptr_t>(x) | (norm ? 0 : reinterpret_cast<uintptr_t>(y))) & 15u) == 0;
-    if (norm) return vec ? launch_pass2_t<true, true>(x, x, n, lut_p2, meta, B, st)
-                         : launch_pass2_t<true, false>(x, x, n, lut_p2, meta, B, st);
-    return vec ? launch_pass2_t<false, true>(x, y, n, lut_p2, meta, B, st)
-               : launch_pass2_t<false, false>(x, y, n, lut_p2, meta, B, st);
+    if (norm) return vec ? launch_pass2_t<true, true>(x, x, n, lut_p2, meta, B, list, list_fill, st)
+                         : launch_pass2_t<true, false>(x, x, n, lut_p2, meta, B, list, list_fill, st);
+    return vec ? launch_pass2_t<false, true>(x, y, n, lut_p2, meta, B, list, list_fill, st)
+               : launch_pass2_t<false, false>(x, y, n, lut_p2, meta, B, list, list_fill, st);
 }
 
 cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,

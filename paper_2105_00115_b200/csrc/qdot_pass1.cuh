@@ -48,6 +48,9 @@ struct __align__(16) P1Shared {
     double2 q[P1_T / 32][32];                // per-warp queue of cold elements (queue mode)
     int base;                                // first key of the private window
     int cbase;                               // first key of the cold window
+    double2* list;                           // this CTA's slot of the cold-element list
+    uint32_t list_fill;                      // entries used in it (across launches)
+    int collect;                             // append cold elements to the list
     int full;                                // this CTA runs the full-variant loop
     int queue;                               // this CTA compacts cold elements through the warp queue
     int kmax;                                // largest sampled key
@@ -93,10 +96,19 @@ __device__ __forceinline__ void exact_variants_signed(double sx, double sy, int3
     kh = __float2int_rn(__fmul_rn(ph, 1024.0f));                                       // units of 2^-10
 }
 
+// append (x, y) to this CTA's slot of the cold-element list (shared counter;
+// no global atomics); an overfull slot is flagged when the CTA ends
+__device__ __forceinline__ void p1_list_append(P1Shared& S, int64_t* __restrict__ A, double xv, double yv) {
+    const uint32_t pos = atomicAdd(&S.list_fill, 1u);
+    if (pos < (uint32_t)LIST_PER_SLOT) S.list[pos] = make_double2(xv, yv);
+}
+
 // cold key: variants from the mantissa bits (mbx, mby = raw bits of mx, my),
-// then the per-CTA limb table or, outside it, global atomics
+// then the per-CTA limb table or, outside it, global atomics; the element
+// itself goes to the cold-element list for a possible pass 2
 __device__ __forceinline__ void p1_cold(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B, int key,
-                                        int64_t kd, uint64_t mbx, uint64_t mby, int32_t sg) {
+                                        int64_t kd, uint64_t mbx, uint64_t mby, int32_t sg, double xv, double yv) {
+    if (S.collect) p1_list_append(S, A, xv, yv);
     int32_t ks, kh;
     exact_variants(bitsd(mbx), bitsd(mby), ks, kh);
     ks = (ks ^ sg) - sg;
@@ -132,7 +144,7 @@ __device__ __noinline__ void p1_special(P1Shared& S, int64_t* __restrict__ A, in
     } else {
         kd = double_units(pb, e);
     }
-    p1_cold(S, A, B, key, kd, mant_bits(bx), mant_bits(by), -(int32_t)((bx ^ by) >> 63));
+    p1_cold(S, A, B, key, kd, mant_bits(bx), mant_bits(by), -(int32_t)((bx ^ by) >> 63), xv, yv);
 }
 
 // one element.  Private-window elements (both factors normal, key in the
@@ -173,7 +185,7 @@ __device__ __forceinline__ bool p1_elem(P1Shared& S, ulonglong2* __restrict__ my
         const int e = (int)esum - 2046;
         const int64_t kd = double_units(dbits(__dmul_rn(xv, yv)), e);
         p1_cold(S, A, B, e + KOFF, kd, (bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull,
-                (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)(hx ^ hy) >> 31);
+                (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)(hx ^ hy) >> 31, xv, yv);
     } else {
         p1_special(S, A, B, xv, yv, zc, nf);
     }
@@ -191,7 +203,7 @@ __device__ __forceinline__ void p1_outside(P1Shared& S, int64_t* __restrict__ A,
         const int e = (int)esum - 2046;
         const int64_t kd = double_units(dbits(__dmul_rn(xv, yv)), e);
         p1_cold(S, A, B, e + KOFF, kd, (bx & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull,
-                (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)(hx ^ hy) >> 31);
+                (by & 0xFFFFFFFFFFFFFull) | 0x3FF0000000000000ull, (int32_t)(hx ^ hy) >> 31, xv, yv);
     } else {
         p1_special(S, A, B, xv, yv, zc, nf);
     }
@@ -517,6 +529,10 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                 }
             }
             S.full = full;
+            const bool slot_ok = blockIdx.x < (unsigned)LIST_SLOTS;
+            S.list = prm.list + (int64_t)(slot_ok ? blockIdx.x : 0) * LIST_PER_SLOT;
+            S.list_fill = slot_ok ? prm.list_fill[blockIdx.x] : (uint32_t)LIST_PER_SLOT;   // no slot: never write
+            S.collect = prm.collect;
             // queue mode when more than 1/128 of the sample lies outside the private window
             const uint32_t ns = pref[KEYS], cov = pref[b + P1_W] - pref[b];
             S.queue = (prm.mode >> 2) == 1 ? 1 : ((prm.mode >> 2) == 2 ? 0 : ((ns - cov) * 128u > ns));
@@ -549,11 +565,24 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     for (int r = tid; r < P1_W; r += P1_T) {
         if (S.t_c[r]) {
             push_key(A, B, S.base + r, (unsigned long long)S.t_c[r], S.t_d[r], S.t_s[r], S.t_h[r]);
+            atomicAdd(reinterpret_cast<unsigned long long*>(A + A_PRIV + S.base + r), (unsigned long long)S.t_c[r]);
             if (!fullmode) atomicAdd(reinterpret_cast<unsigned long long*>(A + A_HOT + S.base + r),
                                      (unsigned long long)S.t_c[r]);
         }
     }
-    if (tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(A + (fullmode ? A_FULLCTAS : A_LEANCTAS)), 1ull);
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(A + (fullmode ? A_FULLCTAS : A_LEANCTAS)), 1ull);
+        const uint32_t f = S.list_fill;
+        if (blockIdx.x < (unsigned)LIST_SLOTS) {
+            const uint32_t before = prm.list_fill[blockIdx.x];
+            prm.list_fill[blockIdx.x] = f;
+            if (f > (uint32_t)LIST_PER_SLOT && before <= (uint32_t)LIST_PER_SLOT)   // flag each slot once
+                atomicAdd(reinterpret_cast<unsigned long long*>(A + A_LISTOVF), 1ull);
+        } else if (f > (uint32_t)LIST_PER_SLOT) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(A + A_LISTOVF), 1ull);
+        }
+    }
     // zero / non-finite counts
     unsigned long long z = zc, f = nf;
     for (int o = 16; o; o >>= 1) {

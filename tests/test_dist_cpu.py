@@ -70,7 +70,7 @@ def _worker(rank, world, port, n, seed, q):
         y = np.ldexp(rng.uniform(0.5, 1, n), rng.integers(-40, 40, n))
         x[rng.integers(0, n, n // 20)] = 0.0
         lo, hi = shard_bounds(n, rank, world)
-        a_len, b_len = 8448, 37760
+        a_len, b_len = 12672, 37760
         A, B = model_regions(x[lo:hi], y[lo:hi], a_len, b_len)
         ta, tb = torch.from_numpy(A), torch.from_numpy(B)
         reduce_regions(ta, tb)

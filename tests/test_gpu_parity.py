@@ -307,3 +307,22 @@ def test_host_inputs_pipelined_equal_device(norm):
             assert r.value == d.value and r.counts == d.counts and r.abs_bound == d.abs_bound
             assert [(q.lower, q.upper, q.cardinality, q.precision) for q in r.params.bins] == \
                    [(q.lower, q.upper, q.cardinality, q.precision) for q in d.params.bins]
+
+
+@pytest.mark.parametrize("strategy,eps", [("ranged:8", 1e-8), ("ranged:2", 1e-8), ("ranged:8", 1e-4), ("ranged:3", 1e-6)])
+def test_pass2_over_cold_list(strategy, eps):
+    # ranged bins whose pass-2 keys all lie outside every private window run
+    # pass 2 over the cold-element list (pass2_needed == 2) instead of a second
+    # stream; either way the result equals the oracle bit for bit
+    from paper_2105_00115_b200.kernel import run_device
+    x, y = O.gen_normal(1 << 21, seed=11)
+    cfg = Q.ToleranceConfig(eps)
+    s = Q.parse_strategy(strategy)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    res, bins, _ = run_device(xd, yd, x.size, False, cfg, s, timing=False)
+    ref = O.qdot(x, y, eps, "none", 52, strategy)
+    got = [(bins[i].lower, bins[i].upper, bins[i].cardinality, bins[i].precision) for i in range(res.n_bins)]
+    assert got == [(b.lower, b.upper, b.cardinality, b.precision) for b in ref.bins]
+    assert res.value == ref.value
+    if strategy in ("ranged:8", "ranged:2") and eps == 1e-8:
+        assert res.pass2_needed == 2
