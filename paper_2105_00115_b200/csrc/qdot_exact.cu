@@ -24,8 +24,6 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
-#include <cstdlib>
-
 #include "qdot_common.cuh"
 
 namespace qd {
@@ -463,17 +461,7 @@ cudaError_t launch_exact_t(const double* x, const double* y, int64_t n, int64_t*
 
 template <bool NORM>
 cudaError_t launch_exact(const double* x, const double* y, int64_t n, int64_t* ws, cudaStream_t st) {
-    static int var = -1;
-    if (var < 0) {
-        const char* e = getenv("QDOT_B200_X_VARIANT");
-        var = e ? atoi(e) : 0;
-    }
-    switch (var) {
-        case 1: return launch_exact_t<NORM, 0>(x, y, n, ws, st);
-        case 2: return launch_exact_t<NORM, 1>(x, y, n, ws, st);
-        case 3: return launch_exact_t<NORM, 6>(x, y, n, ws, st);
-        default: return launch_exact_t<NORM, 3>(x, y, n, ws, st);
-    }
+    return launch_exact_t<NORM, 3>(x, y, n, ws, st);   // bulk L2 prefetch 3 grid-strides ahead
 }
 
 int fail(cudaError_t e, const char* where) { return qd::report_cuda_error(e, where); }
