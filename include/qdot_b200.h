@@ -201,6 +201,19 @@ int qdot_b200_csr_spmv(int64_t n_rows, const int64_t* indptr, const void* indice
 int qdot_b200_vec_update(int64_t n, int op, const double* a, double s, const double* b, double* out,
                          void* stream);
 
+/* device-scalar forms for solver iterations captured in CUDA graphs:
+ * vec_update_dev reads s from device memory; solver_scalar runs one scalar
+ * step on the qdot result in `ws` (which 0: alpha = st[0] / d, st[4] = d;
+ * 1: beta = value / st[0], st[0] = value, st[3] = sqrt(value); 2: st[0] =
+ * value, st[3] = sqrt(value)); publish_iter copies the 256-byte result headers
+ * of ws_a and ws_b and st[0..7] to device-visible pinned host memory (576
+ * bytes) and then writes an incremented sequence word at host + 576. */
+int qdot_b200_vec_update_dev(int64_t n, int op, const double* a, const double* s_dev, const double* b, double* out,
+                             void* stream);
+int qdot_b200_solver_scalar(int which, const void* ws, double* st, void* stream);
+int qdot_b200_publish_iter(const void* ws_a, const void* ws_b, const double* st, void* host, uint32_t* dev_seq,
+                           void* stream);
+
 /* --- exact dot product (verification oracle) --------------------------------- */
 /* Correctly rounded x.y computed exactly on the device: the device form of
  * kernel.reference_dot (kernel.py:98-133) for checking qdot at sizes the host

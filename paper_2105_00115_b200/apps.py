@@ -17,6 +17,13 @@ The generators (gen_stencil, gen_graph_laplacian) build the same CSR matrices
 as the reference on the host; they are input preparation, not the hot path.
 reference_cg / reference_pm are the plain-double baselines (torch on the
 device), kept for iteration-count comparisons like the reference's.
+
+Solves with at least GRAPH_MIN unknowns run every iteration as one CUDA graph
+(SpMV, both qdot pipelines, the scalar recurrence on the device -- alpha,
+beta, sqrt with IEEE division / square root, i.e. the Python float values --
+and the vector updates), whose last node publishes both qdot result headers
+into pinned host memory: one host wake-up per iteration instead of two
+synchronising qdot calls plus separate launches.
 """
 
 from __future__ import annotations
@@ -32,7 +39,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from .binning import ExactBinning, Strategy
-from .device import require_cuda, stream_handle, thread_state
+from .device import config_struct, require_cuda, stream_handle, thread_state
 from .kernel import _raise_status, run_device
 from .scoring import LEVELS_ASC, PrecisionLevel, SplitMode, ToleranceConfig
 
@@ -258,6 +265,102 @@ class PMResult:
     trace: SolveTrace
 
 
+# --------------------------------------------------------------------------- graph iterations
+GRAPH_MIN = 2048          # solves of at least this many unknowns run each iteration as one CUDA graph
+
+
+class _IterGraph:
+    """Device resources of graph-captured solver iterations: two qdot
+    workspaces (one per dot product of an iteration), the scalar state st[8],
+    and a pinned, device-visible host block the last node publishes into
+    (two 256-byte result headers, st, then a sequence word)."""
+
+    def __init__(self, device):
+        torch, _ = _dev()
+        lib = _lib.load()
+        nb = int(lib.qdot_b200_workspace_bytes())
+        self.lib = lib
+        self.ws = [torch.empty(nb, dtype=torch.uint8, device=device) for _ in range(2)]
+        self.st = torch.zeros(8, dtype=torch.float64, device=device)
+        self.seq_dev = torch.zeros(1, dtype=torch.int32, device=device)
+        self.host_t = torch.zeros(640, dtype=torch.uint8).pin_memory()
+        self.host = self.host_t.numpy()
+        self.seq_view = self.host[576:580].view(np.uint32)
+        self.seen = 0
+        self.graphs = []
+
+    def qdot_nodes(self, k: int, xd, yd, norm: bool, c, stream: int) -> None:
+        """The qdot pipeline into workspace k (stream-ordered, no host sync)."""
+        lib, ws, n = self.lib, self.ws[k].data_ptr(), int(xd.shape[0])
+        xp = xd.data_ptr()
+        yp = xp if norm else yd.data_ptr()
+        _lib.check(lib.qdot_b200_begin(ws, stream), lib)
+        _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(norm), ctypes.byref(c), n, ws, stream), lib)
+        _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), stream), lib)
+        _lib.check(lib.qdot_b200_pass2(xp, yp, n, int(norm), ws, stream), lib)
+        _lib.check(lib.qdot_b200_finalize(ws, stream), lib)
+
+    def update(self, op: int, a, si: int, b, out, stream: int) -> None:
+        """out = a + st[si]*b | a - st[si]*b | a / st[si]."""
+        sp = self.st.data_ptr() + 8 * si
+        _lib.check(self.lib.qdot_b200_vec_update_dev(a.shape[0], op, a.data_ptr(), sp,
+                                                     b.data_ptr() if b is not None else None, out.data_ptr(),
+                                                     stream), self.lib)
+
+    def scalar(self, which: int, k: int, stream: int) -> None:
+        _lib.check(self.lib.qdot_b200_solver_scalar(which, self.ws[k].data_ptr(), self.st.data_ptr(), stream),
+                   self.lib)
+
+    def publish(self, stream: int) -> None:
+        _lib.check(self.lib.qdot_b200_publish_iter(self.ws[0].data_ptr(), self.ws[1].data_ptr(), self.st.data_ptr(),
+                                                   self.host_t.data_ptr(), self.seq_dev.data_ptr(), stream),
+                   self.lib)
+
+    def capture(self, body):
+        """Capture `body(stream)` as a CUDA graph on a side stream (nothing runs
+        yet; the launchers' one-time attribute setup is legal during capture).
+        capture_begin/end directly: the torch.cuda.graph context manager would
+        also gc.collect() and empty the caching allocator on every capture."""
+        torch, _ = _dev()
+        self.seen = int(self.seq_view[0])
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            g.capture_begin()
+            try:
+                body(side.cuda_stream)
+            finally:
+                g.capture_end()
+        torch.cuda.current_stream().wait_stream(side)
+        self.graphs.append(g)
+        return g
+
+    def run(self, g):
+        """Replay one iteration and wait for its published block; returns
+        (result header of workspace 0, of workspace 1, st[0..7])."""
+        g.replay()
+        self.seen = (self.seen + 1) & 0xFFFFFFFF
+        torch, _ = _dev()
+        spins = 0
+        while int(self.seq_view[0]) != self.seen:
+            spins += 1
+            if spins & 0xFFFF == 0 and torch.cuda.current_stream().query():
+                if int(self.seq_view[0]) != self.seen:
+                    raise RuntimeError("solver iteration did not publish its result")
+        buf = bytes(self.host[:576])
+        r0 = _lib.QdotResult.from_buffer_copy(buf[0:ctypes.sizeof(_lib.QdotResult)])
+        r1 = _lib.QdotResult.from_buffer_copy(buf[256:256 + ctypes.sizeof(_lib.QdotResult)])
+        st = np.frombuffer(buf[512:576], dtype=np.float64)
+        return r0, r1, st
+
+
+def _dot_report(res) -> "_DotReport":
+    _raise_status(res)
+    counts = {level: int(res.counts[i]) for i, level in enumerate(LEVELS_ASC)}
+    return _DotReport(float(res.value), counts, int(res.n), int(res.zero_count))
+
+
 # --------------------------------------------------------------------------- solvers
 def _norm_dot(dots: _Dots, v):
     rep = dots(v, v, True)
@@ -291,6 +394,39 @@ def acg(a: SparseMatrix, b, x0=None, tau: float = 1e-8, epsilon: float = 1e-8,
     trace.record(0, "rtr", c_rep, resid)
 
     k = 0
+    if n >= GRAPH_MIN and resid > tau and max_iters > 0:
+        # one CUDA graph per iteration: SpMV, p.Ap, alpha, x and r updates, r.r,
+        # beta, p update, publish -- one host wake-up per iteration
+        G = _IterGraph(device)
+        G.st[0] = c
+        cst = config_struct(cfg, strategy)
+
+        def body(stream):
+            a.matvec_device(p, out=q)
+            G.qdot_nodes(0, p, q, False, cst, stream)
+            G.scalar(0, 0, stream)                          # alpha = c / d
+            G.update(_ADD, x, 1, p, x, stream)              # x = x + alpha * p
+            G.update(_SUB, r, 1, q, r, stream)              # r = r - alpha * q
+            G.qdot_nodes(1, r, r, True, cst, stream)
+            G.scalar(1, 1, stream)                          # beta = c_new / c; c = c_new
+            G.update(_ADD, r, 2, p, p, stream)              # p = r + beta * p
+            G.publish(stream)
+
+        g = G.capture(body)
+        while resid > tau and k < max_iters:
+            r_pq, r_rr, st = G.run(g)
+            d_rep = _dot_report(r_pq)
+            d = d_rep.value
+            if not math.isfinite(d) or d <= 0.0:
+                raise BreakdownError(f"p.Ap = {d!r} at iteration {k}")
+            c_rep = _dot_report(r_rr)
+            if not (c_rep.value >= 0.0):                      # apps.py:171-175
+                raise AssertionError("norm computed by qdot must be nonnegative")
+            c = c_rep.value
+            resid = math.sqrt(c)
+            k += 1
+            trace.record(k, "pAp", d_rep, resid)
+            trace.record(k, "rtr", c_rep, resid)
     while resid > tau and k < max_iters:
         a.matvec_device(p, out=q)
         d_rep = dots(p, q, False)
@@ -333,6 +469,45 @@ def apm(a: SparseMatrix, x0, tau: float = 1e-6, epsilon: float = 1e-7, split: Sp
     lam = 0.0
     k = 0
     converged = False
+    if a.n >= GRAPH_MIN and max_iters > 0:
+        # two CUDA graphs (the x / x_next buffers swap roles every iteration):
+        # SpMV, z.z, s = sqrt(z.z), x_next = z / s, x.x_next, publish
+        _, device = _dev()
+        G = _IterGraph(device)
+        cst = config_struct(cfg, strategy)
+        bufs = (x, x_next)
+
+        def body_for(cur, nxt):
+            def body(stream):
+                a.matvec_device(cur, out=z)
+                G.qdot_nodes(0, z, z, True, cst, stream)
+                G.scalar(2, 0, stream)                      # st[0] = z.z, st[3] = sqrt(z.z)
+                G.update(_DIV, z, 3, None, nxt, stream)     # x_next = z / s
+                G.qdot_nodes(1, cur, nxt, False, cst, stream)
+                G.publish(stream)
+            return body
+
+        a.device_arrays()                                   # host->device copies cannot be captured
+        graphs = [G.capture(body_for(bufs[0], bufs[1])), G.capture(body_for(bufs[1], bufs[0]))]
+        while k < max_iters:
+            r_zz, r_lam, _st = G.run(graphs[k % 2])
+            c_rep = _dot_report(r_zz)
+            if c_rep.zero_count == c_rep.n:
+                raise ZeroIterateError(f"A x vanished at iteration {k}")
+            if not (c_rep.value >= 0.0):                      # apps.py:171-175
+                raise AssertionError("norm computed by qdot must be nonnegative")
+            s_ = math.sqrt(c_rep.value)
+            lam_rep = _dot_report(r_lam)
+            lam = lam_rep.value * s_
+            k += 1
+            trace.record(k, "norm", c_rep, lam)
+            trace.record(k, "lambda", lam_rep, lam)
+            if lam_prev is not None and abs(lam - lam_prev) <= tau:
+                converged = True
+                break
+            lam_prev = lam
+        x = bufs[k % 2]
+        return PMResult(eigenvalue=lam, x=x.cpu().numpy(), iterations=k, converged=converged, trace=trace)
     while k < max_iters:
         a.matvec_device(x, out=z)
         # np.any(z) (apps.py:305) from the same qdot call: z.z has a zero

@@ -15,7 +15,7 @@
 
 #include <cstdint>
 
-#include "../../include/qdot_b200.h"
+#include "qdot_common.cuh"
 
 namespace qd {
 int report_cuda_error(cudaError_t e, const char* where);
@@ -87,9 +87,107 @@ __global__ void __launch_bounds__(T) k_read_probe(const double2* __restrict__ x,
     if (acc == 1.2345e-300) *out = acc;     // never true for real data; keeps the loads
 }
 
+// ---- device-side scalar recurrences of the solvers (for CUDA-graph iterations)
+// st: [0] c (r.r, or z.z for the power method), [1] alpha, [2] beta, [3] sqrt(c),
+//     [4] d (p.Ap), [5..7] unused
+__device__ __forceinline__ double result_value(const void* ws) {
+    return reinterpret_cast<const qdot_result*>(static_cast<const char*>(ws) + qd::OFF_RESULT)->value;
+}
+
+// alpha = c / d with d = value of the qdot in ws_pq (apps.py:212-216)
+__global__ void k_cg_alpha(const void* ws_pq, double* st) {
+    const double d = result_value(ws_pq);
+    st[4] = d;
+    st[1] = __ddiv_rn(st[0], d);
+}
+
+// c_new = value of the qdot in ws_rr; beta = c_new / c; c = c_new; sqrt (apps.py:217-223)
+__global__ void k_cg_beta(const void* ws_rr, double* st) {
+    const double c_new = result_value(ws_rr);
+    st[2] = __ddiv_rn(c_new, st[0]);
+    st[0] = c_new;
+    st[3] = __dsqrt_rn(c_new);
+}
+
+// c = value of the qdot in ws; s = sqrt(c) (apps.py:307-309)
+__global__ void k_norm_sqrt(const void* ws, double* st) {
+    const double c = result_value(ws);
+    st[0] = c;
+    st[3] = __dsqrt_rn(c);
+}
+
+// out = a + s*b | a - s*b | a / s with s read from device memory
+template <int OP>
+__global__ void __launch_bounds__(T) k_vec_update_dev(int64_t n, const double* a, const double* __restrict__ sp,
+                                                      const double* b, double* out) {
+    const double s = *sp;
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += (int64_t)gridDim.x * T) {
+        const double av = a[i];
+        double r;
+        if (OP == 0) r = __dadd_rn(av, __dmul_rn(s, b[i]));
+        else if (OP == 1) r = __dsub_rn(av, __dmul_rn(s, b[i]));
+        else r = __ddiv_rn(av, s);
+        out[i] = r;
+    }
+}
+
+// copy the result headers of two qdot workspaces and the scalar state into
+// host memory (pinned, device-visible), then bump the sequence word
+__global__ void k_publish_iter(const void* ws_a, const void* ws_b, const double* st, unsigned char* host,
+                               uint32_t* dev_seq) {
+    const int t = threadIdx.x;
+    const uint32_t* ra = reinterpret_cast<const uint32_t*>(static_cast<const char*>(ws_a) + qd::OFF_RESULT);
+    const uint32_t* rb = reinterpret_cast<const uint32_t*>(static_cast<const char*>(ws_b) + qd::OFF_RESULT);
+    uint32_t* h = reinterpret_cast<uint32_t*>(host);
+    if (t < 64) h[t] = ra[t];                       // 256 B header of ws_a
+    else if (t < 128) h[t] = rb[t - 64];            // 256 B header of ws_b
+    else if (t < 144) h[t] = reinterpret_cast<const uint32_t*>(st)[t - 128];   // 64 B state
+    __threadfence_system();
+    __syncthreads();
+    if (t == 0) {
+        const uint32_t sq = *dev_seq + 1;
+        *dev_seq = sq;
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(host + 576) = sq;
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+int qdot_b200_vec_update_dev(int64_t n, int op, const double* a, const double* s_dev, const double* b, double* out,
+                             void* stream) {
+    if (n < 0 || op < 0 || op > 2 || !s_dev) return QDOT_ERR_ARG;
+    if (n == 0) return QDOT_OK;
+    if (!a || !out || (op != 2 && !b)) return QDOT_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int g = grid_for(n, 4);
+    if (op == 0) k_vec_update_dev<0><<<g, T, 0, st>>>(n, a, s_dev, b, out);
+    else if (op == 1) k_vec_update_dev<1><<<g, T, 0, st>>>(n, a, s_dev, b, out);
+    else k_vec_update_dev<2><<<g, T, 0, st>>>(n, a, s_dev, b, out);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "vec_update_dev");
+}
+
+int qdot_b200_solver_scalar(int which, const void* ws, double* st, void* stream) {
+    if (!ws || !st || which < 0 || which > 2) return QDOT_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (which == 0) k_cg_alpha<<<1, 1, 0, s>>>(ws, st);
+    else if (which == 1) k_cg_beta<<<1, 1, 0, s>>>(ws, st);
+    else k_norm_sqrt<<<1, 1, 0, s>>>(ws, st);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "solver_scalar");
+}
+
+int qdot_b200_publish_iter(const void* ws_a, const void* ws_b, const double* st, void* host, uint32_t* dev_seq,
+                           void* stream) {
+    if (!ws_a || !ws_b || !st || !host || !dev_seq) return QDOT_ERR_ARG;
+    k_publish_iter<<<1, 160, 0, static_cast<cudaStream_t>(stream)>>>(ws_a, ws_b, st,
+                                                                      static_cast<unsigned char*>(host), dev_seq);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "publish_iter");
+}
 
 int qdot_b200_read_probe(const double* x, int64_t n, double* out, void* stream) {
     if (n < 0 || (n > 0 && (!x || !out)) || (reinterpret_cast<uintptr_t>(x) & 15u)) return QDOT_ERR_ARG;

@@ -39,8 +39,18 @@ def csv_sha(tr):
     return hashlib.sha256(b.getvalue().encode()).hexdigest()[:16]
 
 
+@pytest.fixture(params=["eager", "graph"])
+def iteration_mode(request, monkeypatch):
+    # "graph": every solve, however small, runs its iterations as CUDA graphs
+    if request.param == "graph":
+        monkeypatch.setattr(apps, "GRAPH_MIN", 1)
+    else:
+        monkeypatch.setattr(apps, "GRAPH_MIN", 1 << 62)
+    return request.param
+
+
 @pytest.mark.parametrize("case", U.golden()["cg"], ids=lambda c: c["name"])
-def test_acg_golden(case):
+def test_acg_golden(case, iteration_mode):
     a, rhs = U.matrix(case["matrix"])
     bspec = case["opts"].get("b")
     b = rhs if bspec is None else {"arange": np.arange(1.0, a.n + 1.0), "zeros": np.zeros(a.n),
@@ -61,7 +71,7 @@ def test_acg_golden(case):
 
 
 @pytest.mark.parametrize("case", U.golden()["pm"], ids=lambda c: c["name"])
-def test_apm_golden(case):
+def test_apm_golden(case, iteration_mode):
     a, _ = U.matrix(case["matrix"])
     x0 = U.x0_for(case["x0"], a.n)
     assert U.sha(x0) == case["x0_sha"]
