@@ -348,6 +348,31 @@ int qdot_b200_dot(const double* x, const double* y, int64_t n, int norm, const q
     return collect(st, ws, out, bins, max_bins);
 }
 
+// per-host-thread device buffers, workspace, streams and chunk events of the
+// host-input path (grow-only; released at thread exit)
+namespace {
+struct HostPath {
+    int dev = -1;
+    double* dx = nullptr;
+    double* dy = nullptr;
+    int64_t cap = 0;
+    void* ws = nullptr;
+    cudaStream_t cs = nullptr, ks = nullptr;
+    std::vector<cudaEvent_t> evs;
+    void release() {
+        for (auto ev : evs) cudaEventDestroy(ev);
+        evs.clear();
+        if (cs) cudaStreamDestroy(cs);
+        if (ks) cudaStreamDestroy(ks);
+        cudaFree(dx); cudaFree(dy); cudaFree(ws);
+        dx = dy = nullptr; ws = nullptr; cs = ks = nullptr; cap = 0;
+    }
+    ~HostPath() { release(); }
+};
+thread_local HostPath g_host;
+constexpr int64_t HOST_CHUNK = 1ll << 22;   // elements per overlapped chunk
+}  // namespace
+
 int qdot_b200_dot_host(const double* hx, const double* hy, int64_t n, int norm, const qdot_config* cfg,
                        qdot_result* out, qdot_bin* bins, int32_t max_bins) {
     int v = validate(cfg);
@@ -355,51 +380,54 @@ int qdot_b200_dot_host(const double* hx, const double* hy, int64_t n, int norm, 
     if (n < 0 || (n > 0 && (!hx || (!norm && !hy)))) return QDOT_ERR_ARG;
     int sm = 0;
     if ((v = qdot_b200_device_info(&sm, nullptr, nullptr))) return v;
-    double *dx = nullptr, *dy = nullptr;
-    void* ws = nullptr;
-    cudaStream_t cs = nullptr, ks = nullptr;
-    std::vector<cudaEvent_t> evs;
-    int rc = QDOT_OK;
+    int dev = 0;
+    QD_CHECK(cudaGetDevice(&dev), "cudaGetDevice");
+    HostPath& H = g_host;
+    if (H.dev != dev) { H.release(); H.dev = dev; }
     const int64_t nb = n > 0 ? n : 1;
-    const int64_t CH = 1ll << 22;   // elements per overlapped chunk
-    auto fail = [&](cudaError_t e, const char* w) { rc = cuda_fail(e, w); };
-    cudaError_t e;
-    if ((e = cudaMalloc(&dx, sizeof(double) * nb)) != cudaSuccess) { fail(e, "malloc x"); goto out_; }
-    if (!norm && (e = cudaMalloc(&dy, sizeof(double) * nb)) != cudaSuccess) { fail(e, "malloc y"); goto out_; }
-    if ((e = cudaMalloc(&ws, WS_BYTES)) != cudaSuccess) { fail(e, "malloc ws"); goto out_; }
-    if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking)) != cudaSuccess) { fail(e, "stream"); goto out_; }
-    if ((e = cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking)) != cudaSuccess) { fail(e, "stream"); goto out_; }
-    if ((rc = qdot_b200_begin(ws, ks))) goto out_;
-    // copy chunk c on the copy stream while pass 1 consumes chunk c-1
-    for (int64_t off = 0; off < n; off += CH) {
-        int64_t len = n - off < CH ? n - off : CH;
-        cudaEvent_t ev;
-        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) { fail(e, "event"); goto out_; }
-        evs.push_back(ev);
-        if ((e = cudaMemcpyAsync(dx + off, hx + off, sizeof(double) * len, cudaMemcpyHostToDevice, cs)) != cudaSuccess) {
-            fail(e, "H2D x"); goto out_;
-        }
-        if (!norm && (e = cudaMemcpyAsync(dy + off, hy + off, sizeof(double) * len, cudaMemcpyHostToDevice, cs)) !=
-                         cudaSuccess) {
-            fail(e, "H2D y"); goto out_;
-        }
-        cudaEventRecord(ev, cs);
-        cudaStreamWaitEvent(ks, ev, 0);
-        if ((rc = qdot_b200_pass1(dx + off, norm ? nullptr : dy + off, len, norm, cfg, n, ws, ks))) goto out_;
+    if (nb > H.cap) {
+        cudaFree(H.dx); cudaFree(H.dy);
+        H.dx = H.dy = nullptr; H.cap = 0;
+        QD_CHECK(cudaMalloc(&H.dx, sizeof(double) * nb), "malloc x");
+        QD_CHECK(cudaMalloc(&H.dy, sizeof(double) * nb), "malloc y");
+        H.cap = nb;
     }
-    if ((rc = qdot_b200_score_finalize(ws, n, cfg, ks))) goto out_;
-    if ((rc = qdot_b200_pass2(dx, norm ? nullptr : dy, n, norm, ws, ks))) goto out_;
-    if ((rc = qdot_b200_finalize(ws, ks))) goto out_;
-    rc = qdot_b200_fetch(ws, out, bins, max_bins, ks);
-out_:
-    if (ks) cudaStreamSynchronize(ks);
-    if (cs) cudaStreamSynchronize(cs);
-    for (auto ev : evs) cudaEventDestroy(ev);
-    if (cs) cudaStreamDestroy(cs);
-    if (ks) cudaStreamDestroy(ks);
-    cudaFree(dx);
-    cudaFree(dy);
-    cudaFree(ws);
+    if (!H.ws) QD_CHECK(cudaMalloc(&H.ws, WS_BYTES), "malloc ws");
+    if (!H.cs) QD_CHECK(cudaStreamCreateWithFlags(&H.cs, cudaStreamNonBlocking), "stream");
+    if (!H.ks) QD_CHECK(cudaStreamCreateWithFlags(&H.ks, cudaStreamNonBlocking), "stream");
+    const int64_t nchunks = (n + HOST_CHUNK - 1) / HOST_CHUNK;
+    while ((int64_t)H.evs.size() < nchunks) {
+        cudaEvent_t ev;
+        QD_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        H.evs.push_back(ev);
+    }
+    double *dx = H.dx, *dy = H.dy;
+    void* ws = H.ws;
+    cudaStream_t cs = H.cs, ks = H.ks;
+    int rc = QDOT_OK;
+    if ((rc = qdot_b200_begin(ws, ks))) return rc;
+    // the copy stream starts after the previous call's kernels are done with the buffers
+    if (!H.evs.empty()) {
+        QD_CHECK(cudaEventRecord(H.evs[0], ks), "event");
+        QD_CHECK(cudaStreamWaitEvent(cs, H.evs[0], 0), "wait");
+    }
+    // copy chunk c on the copy stream while pass 1 consumes chunk c-1
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t off = c * HOST_CHUNK;
+        const int64_t len = n - off < HOST_CHUNK ? n - off : HOST_CHUNK;
+        QD_CHECK(cudaMemcpyAsync(dx + off, hx + off, sizeof(double) * len, cudaMemcpyHostToDevice, cs), "H2D x");
+        if (!norm)
+            QD_CHECK(cudaMemcpyAsync(dy + off, hy + off, sizeof(double) * len, cudaMemcpyHostToDevice, cs), "H2D y");
+        QD_CHECK(cudaEventRecord(H.evs[c], cs), "event");
+        QD_CHECK(cudaStreamWaitEvent(ks, H.evs[c], 0), "wait");
+        if ((rc = qdot_b200_pass1(dx + off, norm ? nullptr : dy + off, len, norm, cfg, n, ws, ks))) break;
+    }
+    if (!rc) rc = qdot_b200_score_finalize(ws, n, cfg, ks);
+    if (!rc) rc = qdot_b200_pass2(dx, norm ? nullptr : dy, n, norm, ws, ks);
+    if (!rc) rc = qdot_b200_finalize(ws, ks);
+    if (!rc) rc = qdot_b200_fetch(ws, out, bins, max_bins, ks);
+    cudaStreamSynchronize(ks);
+    cudaStreamSynchronize(cs);
     return rc;
 }
 

@@ -326,3 +326,34 @@ def test_pass2_over_cold_list(strategy, eps):
     assert res.value == ref.value
     if strategy in ("ranged:8", "ranged:2") and eps == 1e-8:
         assert res.pass2_needed == 2
+
+
+@pytest.mark.parametrize("n,norm", [(0, False), (1000, False), ((1 << 22) + 12345, False), ((1 << 22) + 7, True),
+                                    (3 * (1 << 22), False)])
+def test_c_abi_dot_host(n, norm):
+    # the one-call host-buffer entry point of the C ABI (what an FFI binding uses)
+    import ctypes
+    from paper_2105_00115_b200 import _lib
+    from paper_2105_00115_b200.device import config_struct
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n)
+    y = x if norm else rng.standard_normal(n)
+    cfg = Q.ToleranceConfig(1e-7, Q.SplitMode.PER_BIN)
+    lib = _lib.load()
+    c = config_struct(cfg, Q.RangedBinning(2))
+    res = _lib.QdotResult()
+    bins = (_lib.QdotBin * (_lib.KEYS + 1))()
+    dp = ctypes.POINTER(ctypes.c_double)
+    for _ in range(2):   # second call reuses the cached buffers
+        _lib.check(lib.qdot_b200_dot_host(x.ctypes.data_as(dp) if n else None,
+                                          y.ctypes.data_as(dp) if n else None, n, int(norm), ctypes.byref(c),
+                                          ctypes.byref(res), bins, _lib.KEYS + 1), lib)
+        if n == 0:
+            assert res.value == 0.0 and res.n_bins == 0
+            continue
+        xd = torch.from_numpy(x).cuda()
+        yd = xd if norm else torch.from_numpy(y).cuda()
+        rep = Q.qdot(xd, yd, cfg, strategy=Q.RangedBinning(2))
+        assert res.value == rep.value and res.n_bins == len(rep.params.bins)
+        assert [(bins[i].lower, bins[i].upper, bins[i].cardinality) for i in range(res.n_bins)] == \
+               [(b.lower, b.upper, b.cardinality) for b in rep.params.bins]
