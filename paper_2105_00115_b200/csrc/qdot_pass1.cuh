@@ -431,114 +431,153 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     constexpr int TILE = P1_T * 2 * V;
     const int64_t ntiles = (n + TILE - 1) / TILE;
 
-    // ---- sample this CTA's first tile: histogram of keys (reusing priv)
-    uint32_t* hist = reinterpret_cast<uint32_t*>(S.priv);           // KEYS u32
-    uint32_t* pref = hist + 4224;                                   // KEYS+1 u32
-    for (int k = tid; k < 4224 * 2; k += P1_T) hist[k] = 0u;
-    __syncthreads();
-    if ((int64_t)blockIdx.x < ntiles) {
-        double xv[2 * V], yv[2 * V];
-        bool full;
-        p1_load<NORM, VEC, V>(x, y, n, blockIdx.x, tid, xv, yv, full);
-        const int64_t e0 = (int64_t)blockIdx.x * TILE;
-#pragma unroll
-        for (int j = 0; j < 2 * V; ++j) {
-            int64_t i = e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1);
-            if (i >= n) continue;
-            uint64_t bx = dbits(xv[j]), by = dbits(yv[j]);
-            uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
-            if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) atomicAdd(&hist[(int)(fx + fy) - 2046 + KOFF], 1u);
-        }
-    }
-    __syncthreads();
-    {   // inclusive prefix over KEYS (17 keys per thread) + largest sampled key
-        constexpr int PER = (KEYS + P1_T - 1) / P1_T;
-        uint32_t loc[PER];
-        uint32_t run = 0;
+    if (SMALL) {
+        // short inputs: the window only has to be reasonable -- [kmax - W + 3,
+        // kmax + 2] around the largest key of the first tile (no histogram)
         int kmx = -1;
+        if ((int64_t)blockIdx.x < ntiles) {
+            double xv[2 * V], yv[2 * V];
+            bool full;
+            p1_load<NORM, VEC, V>(x, y, n, blockIdx.x, tid, xv, yv, full);
+            const int64_t e0 = (int64_t)blockIdx.x * TILE;
 #pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            int k = tid * PER + i;
-            uint32_t h = k < KEYS ? hist[k] : 0u;
-            if (h) kmx = k;
-            run += h;
-            loc[i] = run;
+            for (int j = 0; j < 2 * V; ++j) {
+                const int64_t i = e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1);
+                const uint32_t fx = (uint32_t)(dbits(xv[j]) >> 52) & 0x7FFu, fy = (uint32_t)(dbits(yv[j]) >> 52) & 0x7FFu;
+                if (i < n && fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) kmx = max(kmx, (int)(fx + fy) - 2046 + KOFF);
+            }
         }
-        const int lane = tid & 31, warp = tid >> 5;
-        uint32_t incl = run;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        for (int o = 16; o; o >>= 1) kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
-        if (lane == 31) S.red[warp] = incl;
-        if (lane == 0) S.red[P1_T / 32 + warp] = (unsigned long long)(long long)kmx;
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        if ((tid & 31) == 0) S.red[tid >> 5] = (unsigned long long)(long long)kmx;
         __syncthreads();
-        uint32_t wpre = 0;
-        for (int w = 0; w < warp; ++w) wpre += (uint32_t)S.red[w];
-        uint32_t pre = wpre + incl - run;
-        pref[0] = 0u;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            int k = tid * PER + i;
-            if (k < KEYS) pref[k + 1] = pre + loc[i];
-        }
         if (tid == 0) {
             int m = -1;
-            for (int w = 0; w < P1_T / 32; ++w) m = max(m, (int)(long long)S.red[P1_T / 32 + w]);
+            for (int w = 0; w < P1_T / 32; ++w) m = max(m, (int)(long long)S.red[w]);
+            int b = m < 0 ? KOFF - 8 : m - P1_W + 3;
+            b = b < P1_SAFE_LO ? P1_SAFE_LO : (b > P1_SAFE_HI ? P1_SAFE_HI : b);
             S.kmax = m;
-        }
-    }
-    __syncthreads();
-    {   // private window: argmax over starts b of pref[b+W] - pref[b], inside the safe range
-        unsigned long long best = 0ull;
-        for (int b = P1_SAFE_LO + tid; b <= P1_SAFE_HI; b += P1_T) {
-            uint32_t s = pref[b + P1_W] - pref[b];
-            unsigned long long cand = ((unsigned long long)s << 32) | (uint32_t)(0xFFFFFFFFu - b);
-            best = cand > best ? cand : best;
-        }
-        for (int o = 16; o; o >>= 1) {
-            unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
-            best = t > best ? t : best;
-        }
-        __syncthreads();
-        if ((tid & 31) == 0) S.red[tid >> 5] = best;
-        __syncthreads();
-        if (tid == 0) {
-            unsigned long long m = 0ull;
-            for (int w = 0; w < P1_T / 32; ++w) m = S.red[w] > m ? S.red[w] : m;
-            int b = (m >> 32) ? (int)(0xFFFFFFFFu - (uint32_t)m) : (KOFF - 8);   // default near e = 0
             S.base = b;
             int cb = b - (P1_CW - P1_W) / 2;
             cb = cb < 0 ? 0 : cb;
-            cb = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
-            S.cbase = cb;
-            // lean / full decision (see header); only speed depends on it
-            int full = 0;
-            if (SMALL || (prm.mode & 3) == 2 || prm.input_mu != 52) full = 1;
-            else if ((prm.mode & 3) == 0) {
-                const uint32_t ns = pref[KEYS];
-                const int fl = flexp_bits(dbits(prm.epsilon));
-                for (int r = 0; r < P1_W && ns; ++r) {
-                    uint32_t c = hist[b + r];
-                    if (!c) continue;
-                    double mest = (double)c * (double)prm.n_total / (double)ns;
-                    int lg = mest >= 1.0 ? flexp_bits(dbits(mest)) : 0;
-                    int score = lg - 2 + (b + r - S.kmax) - fl + 1;
-                    if (score > -6 && score < 27) full = 1;
-                }
-            }
-            S.full = full;
+            S.cbase = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
+            S.full = 1;
+            S.queue = 0;
             const bool slot_ok = blockIdx.x < (unsigned)LIST_SLOTS;
             S.list = prm.list + (int64_t)(slot_ok ? blockIdx.x : 0) * LIST_PER_SLOT;
-            S.list_fill = slot_ok ? prm.list_fill[blockIdx.x] : (uint32_t)LIST_PER_SLOT;   // no slot: never write
+            S.list_fill = slot_ok ? prm.list_fill[blockIdx.x] : (uint32_t)LIST_PER_SLOT;
             S.collect = prm.collect;
-            // queue mode when more than 1/128 of the sample lies outside the private window
-            const uint32_t ns = pref[KEYS], cov = pref[b + P1_W] - pref[b];
-            S.queue = (prm.mode >> 2) == 1 ? 1 : ((prm.mode >> 2) == 2 ? 0 : ((ns - cov) * 128u > ns));
         }
+        __syncthreads();
+    } else {
+        // ---- sample this CTA's first tile: histogram of keys (reusing priv)
+        uint32_t* hist = reinterpret_cast<uint32_t*>(S.priv);           // KEYS u32
+        uint32_t* pref = hist + 4224;                                   // KEYS+1 u32
+        for (int k = tid; k < 4224 * 2; k += P1_T) hist[k] = 0u;
+        __syncthreads();
+        if ((int64_t)blockIdx.x < ntiles) {
+            double xv[2 * V], yv[2 * V];
+            bool full;
+            p1_load<NORM, VEC, V>(x, y, n, blockIdx.x, tid, xv, yv, full);
+            const int64_t e0 = (int64_t)blockIdx.x * TILE;
+    #pragma unroll
+            for (int j = 0; j < 2 * V; ++j) {
+                int64_t i = e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1);
+                if (i >= n) continue;
+                uint64_t bx = dbits(xv[j]), by = dbits(yv[j]);
+                uint32_t fx = (uint32_t)(bx >> 52) & 0x7FFu, fy = (uint32_t)(by >> 52) & 0x7FFu;
+                if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) atomicAdd(&hist[(int)(fx + fy) - 2046 + KOFF], 1u);
+            }
+        }
+        __syncthreads();
+        {   // inclusive prefix over KEYS (17 keys per thread) + largest sampled key
+            constexpr int PER = (KEYS + P1_T - 1) / P1_T;
+            uint32_t loc[PER];
+            uint32_t run = 0;
+            int kmx = -1;
+    #pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                int k = tid * PER + i;
+                uint32_t h = k < KEYS ? hist[k] : 0u;
+                if (h) kmx = k;
+                run += h;
+                loc[i] = run;
+            }
+            const int lane = tid & 31, warp = tid >> 5;
+            uint32_t incl = run;
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            for (int o = 16; o; o >>= 1) kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, o));
+            if (lane == 31) S.red[warp] = incl;
+            if (lane == 0) S.red[P1_T / 32 + warp] = (unsigned long long)(long long)kmx;
+            __syncthreads();
+            uint32_t wpre = 0;
+            for (int w = 0; w < warp; ++w) wpre += (uint32_t)S.red[w];
+            uint32_t pre = wpre + incl - run;
+            pref[0] = 0u;
+    #pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                int k = tid * PER + i;
+                if (k < KEYS) pref[k + 1] = pre + loc[i];
+            }
+            if (tid == 0) {
+                int m = -1;
+                for (int w = 0; w < P1_T / 32; ++w) m = max(m, (int)(long long)S.red[P1_T / 32 + w]);
+                S.kmax = m;
+            }
+        }
+        __syncthreads();
+        {   // private window: argmax over starts b of pref[b+W] - pref[b], inside the safe range
+            unsigned long long best = 0ull;
+            for (int b = P1_SAFE_LO + tid; b <= P1_SAFE_HI; b += P1_T) {
+                uint32_t s = pref[b + P1_W] - pref[b];
+                unsigned long long cand = ((unsigned long long)s << 32) | (uint32_t)(0xFFFFFFFFu - b);
+                best = cand > best ? cand : best;
+            }
+            for (int o = 16; o; o >>= 1) {
+                unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+                best = t > best ? t : best;
+            }
+            __syncthreads();
+            if ((tid & 31) == 0) S.red[tid >> 5] = best;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long m = 0ull;
+                for (int w = 0; w < P1_T / 32; ++w) m = S.red[w] > m ? S.red[w] : m;
+                int b = (m >> 32) ? (int)(0xFFFFFFFFu - (uint32_t)m) : (KOFF - 8);   // default near e = 0
+                S.base = b;
+                int cb = b - (P1_CW - P1_W) / 2;
+                cb = cb < 0 ? 0 : cb;
+                cb = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
+                S.cbase = cb;
+                // lean / full decision (see header); only speed depends on it
+                int full = 0;
+                if (SMALL || (prm.mode & 3) == 2 || prm.input_mu != 52) full = 1;
+                else if ((prm.mode & 3) == 0) {
+                    const uint32_t ns = pref[KEYS];
+                    const int fl = flexp_bits(dbits(prm.epsilon));
+                    for (int r = 0; r < P1_W && ns; ++r) {
+                        uint32_t c = hist[b + r];
+                        if (!c) continue;
+                        double mest = (double)c * (double)prm.n_total / (double)ns;
+                        int lg = mest >= 1.0 ? flexp_bits(dbits(mest)) : 0;
+                        int score = lg - 2 + (b + r - S.kmax) - fl + 1;
+                        if (score > -6 && score < 27) full = 1;
+                    }
+                }
+                S.full = full;
+                const bool slot_ok = blockIdx.x < (unsigned)LIST_SLOTS;
+                S.list = prm.list + (int64_t)(slot_ok ? blockIdx.x : 0) * LIST_PER_SLOT;
+                S.list_fill = slot_ok ? prm.list_fill[blockIdx.x] : (uint32_t)LIST_PER_SLOT;   // no slot: never write
+                S.collect = prm.collect;
+                // queue mode when more than 1/128 of the sample lies outside the private window
+                const uint32_t ns = pref[KEYS], cov = pref[b + P1_W] - pref[b];
+                S.queue = (prm.mode >> 2) == 1 ? 1 : ((prm.mode >> 2) == 2 ? 0 : ((ns - cov) * 128u > ns));
+            }
+        }
+        __syncthreads();
     }
-    __syncthreads();
     // ---- clear private slots, cold table and totals
     for (int k = tid; k < P1_W * P1_T; k += P1_T) S.priv[k] = make_ulonglong2(0ull, 0ull);
     for (int k = tid; k < P1_CW; k += P1_T) {
