@@ -46,6 +46,7 @@ struct ScShared {
     int s_status, s_deg, s_early, s_nb, s_need;
     int kmin, kmax;
     long long nnz;
+    long long a_zero, a_listovf;
     double eps_eff;
     long long fl;
 };
@@ -141,6 +142,9 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
     ScShared& S = *reinterpret_cast<ScShared*>(smem_raw);
     const int tid = threadIdx.x;
 
+    // the flag words are loaded up front so their latency overlaps the counts'
+    long long a_nonfinite = 0, a_zero = 0, a_listovf = 0;
+    if (tid == 0) { a_nonfinite = A[A_NONFINITE]; a_zero = A[A_ZERO]; a_listovf = A[A_LISTOVF]; }
     unsigned long long cnt[SC_PER];
     int kmin = KEYS, kmax = -1;
     unsigned long long tot = 0;
@@ -151,8 +155,15 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         if (cnt[i]) { kmin = min(kmin, k); kmax = max(kmax, k); }
         tot += cnt[i];
     }
-    kmin = block_reduce<int>(kmin, reinterpret_cast<int*>(S.red2), [](int a, int b) { return a < b ? a : b; }, KEYS);
-    kmax = block_reduce<int>(kmax, reinterpret_cast<int*>(S.red2), [](int a, int b) { return a > b ? a : b; }, -1);
+    {   // one reduction for both, component-wise min of (kmin, KEYS - kmax) in 16-bit halves
+        const unsigned packed = ((unsigned)kmin << 16) | (unsigned)(KEYS - kmax);
+        const unsigned r = block_reduce<unsigned>(
+            packed, reinterpret_cast<unsigned*>(S.red2),
+            [](unsigned a, unsigned b) { return (min(a >> 16, b >> 16) << 16) | min(a & 0xFFFFu, b & 0xFFFFu); },
+            0xFFFFFFFFu);
+        kmin = (int)(r >> 16);
+        kmax = KEYS - (int)(r & 0xFFFFu);
+    }
     // exclusive prefix of counts -> off[]
     unsigned long long ex[SC_PER];
 #pragma unroll
@@ -168,7 +179,7 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
 
     if (tid == 0) {
         int status = QDOT_OK;
-        if (A[A_NONFINITE]) status = QDOT_ERR_NONFINITE;                          // floatbits.py:70
+        if (a_nonfinite) status = QDOT_ERR_NONFINITE;                             // floatbits.py:70
         int deg = nnz == 0;
         int early = 0;
         bool ok = true;
@@ -180,6 +191,7 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         }
         S.s_status = status; S.s_deg = deg; S.s_early = early;
         S.kmin = kmin; S.kmax = kmax; S.nnz = (long long)nnz;
+        S.a_zero = a_zero; S.a_listovf = a_listovf;
     }
     __syncthreads();
     const int deg = S.s_deg, early = S.s_early;
@@ -307,8 +319,11 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
     __threadfence_block();
     // ---- LUTs.  need: some key needs pass 2; priv: such a key also has
     // elements accumulated in private windows (not in the cold-element list)
+    // only keys in [kmin, kmax] are ever looked up (pass 2 by element keys,
+    // finalize by bin keys), so stale entries outside the range are harmless
     int need = 0, priv = 0;
-    for (int k = tid; k < KEYS; k += SC_T) {
+    const int lut_lo = deg ? 0 : S.kmin, lut_hi = deg ? -1 : S.kmax;
+    for (int k = lut_lo + tid; k <= lut_hi; k += SC_T) {
         int b = S.bin_of[k];
         lut_bin[k] = b;
         uint32_t d = 0;
@@ -329,14 +344,14 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
     priv = block_reduce<int>(priv, reinterpret_cast<int*>(S.red2), [](int a, int b) { return a | b; }, 0);
     // pass 2 mode: 2 = only over the cold-element list (every element of every
     // pass-2 key is in it, no slot overflowed), 1 = stream x and y again
-    if (need) need = (!priv && A[A_LISTOVF] == 0) ? 2 : 1;
+    if (need) need = (!priv && S.a_listovf == 0) ? 2 : 1;
     __shared__ ScoreMeta sm;
     if (tid == 0) {
         ScoreMeta m;
         m.status = S.s_status; m.n_bins = nb; m.e_min = e_min; m.e_max = e_max;
         m.early = early; m.need_p2 = need; m.degenerate = deg; m.input_mu = cfg.input_mu;
         m.done = (fuse && !need) ? 1 : 0; m.pad_ = 0;
-        m.nnz = S.nnz; m.zero = A[A_ZERO]; m.n_total = n_total; m.eps_eff = S.eps_eff;
+        m.nnz = S.nnz; m.zero = S.a_zero; m.n_total = n_total; m.eps_eff = S.eps_eff;
         sm = m;
         *meta = m;
     }
