@@ -137,8 +137,9 @@ int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const
         prm.epsilon = cfg->epsilon;
         prm.input_mu = cfg->input_mu;
         prm.collect = cfg->strategy != QDOT_STRATEGY_EXACT;
-        prm.mode = cfg->reserved;   // bits 0-1: 0 auto, 1 lean, 2 full; bits 2-3: queue 0 auto, 4 on, 8 off
-        if (prm.mode < 0 || (prm.mode & 3) > 2 || (prm.mode >> 2) > 2) return QDOT_ERR_ARG;
+        // bits 0-1: 0 auto, 1 lean, 2 full; bits 2-3: queue 0 auto, 4 on, 8 off; bit 4: wide lean window
+        prm.mode = cfg->reserved;
+        if (prm.mode < 0 || (prm.mode & 3) > 2 || ((prm.mode >> 2) & 3) > 2 || (prm.mode >> 5)) return QDOT_ERR_ARG;
     }
     WsPtrs w = ws_ptrs(ws);
     QD_CHECK(launch_pass1(x, norm ? x : y, n, norm != 0, w.a, w.b, prm, static_cast<cudaStream_t>(stream)), "pass1");

@@ -30,16 +30,18 @@
 
 constexpr int P1_T = 256;                    // threads per CTA
 constexpr int P1_W = 16;                     // keys with per-thread private slots
+constexpr int P1_WW = 24;                    // wide lean window: {D int64, count u16} per (key, thread)
 constexpr int P1_CW = 128;                   // keys with per-CTA 32-bit limb tables
 // private window keys keep e in [-971, 1021]: fl(x*y) normal and finite and
 // 2^(52-e) representable
 constexpr int P1_SAFE_LO = KOFF - 971;
 constexpr int P1_SAFE_HI = KOFF + 1021 - P1_W + 1;
+constexpr int P1_SAFE_HI_W = KOFF + 1021 - P1_WW + 1;
 
 struct __align__(16) P1Shared {
     ulonglong2 priv[P1_W * P1_T];            // lean: {D, count}; full: {D, packed S|H|count}
-    __int128 t_d[P1_W];                      // CTA totals of the private window
-    long long t_s[P1_W], t_h[P1_W], t_c[P1_W];
+    __int128 t_d[P1_WW];                     // CTA totals of the private window
+    long long t_s[P1_WW], t_h[P1_WW], t_c[P1_WW];
     // cold window, 32-bit limbs: D = d0 + d1 2^14 + d2 2^28 + d3 2^42 (d3 signed),
     // S = s0 + s1 2^14 (s1 signed), H (signed)
     uint32_t c_cnt[P1_CW], c_d0[P1_CW], c_d1[P1_CW], c_d2[P1_CW], c_d3[P1_CW];
@@ -52,6 +54,7 @@ struct __align__(16) P1Shared {
     uint32_t list_fill;                      // entries used in it (across launches)
     int collect;                             // append cold elements to the list
     int full;                                // this CTA runs the full-variant loop
+    int wide;                                // lean loop over the 24-key window
     int queue;                               // this CTA compacts cold elements through the warp queue
     int kmax;                                // largest sampled key
 };
@@ -152,7 +155,9 @@ __device__ __noinline__ void p1_special(P1Shared& S, int64_t* __restrict__ A, in
 // integer in [2^52, 2^54] -> one conversion gives the signed DOUBLE units.
 // QUEUE: elements outside the private window are not handled here; the
 // return value flags them for the warp queue.
-template <bool FULL, bool QUEUE>
+// WW == P1_WW: the wide lean layout (FULL is false): per (key, thread) an
+// int64 DOUBLE sum in priv[0 .. 24*256) as long long and a u16 count after it.
+template <bool FULL, bool QUEUE, int WW = P1_W>
 __device__ __forceinline__ bool p1_elem(P1Shared& S, ulonglong2* __restrict__ my, int kbias,
                                         int64_t* __restrict__ A, int64_t* __restrict__ B, double xv, double yv,
                                         uint32_t* zc, uint32_t* nf) {
@@ -160,8 +165,15 @@ __device__ __forceinline__ bool p1_elem(P1Shared& S, ulonglong2* __restrict__ my
     const uint32_t fx = (hx >> 20) & 0x7FFu, fy = (hy >> 20) & 0x7FFu;
     const uint32_t esum = fx + fy;                                      // e + 2046
     const int rel = (int)esum + kbias;                                  // key - base
-    const bool hot = (max(fx - 1u, fy - 1u) < 0x7FEu) & ((unsigned)rel < (unsigned)P1_W);
-    if (hot) {
+    const bool hot = (max(fx - 1u, fy - 1u) < 0x7FEu) & ((unsigned)rel < (unsigned)WW);
+    if (WW == P1_WW && hot) {
+        const double scale = __hiloint2double((int)((3121u - esum) << 20), 0);   // 2^(52-e)
+        const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv, yv), scale));
+        long long* wd = reinterpret_cast<long long*>(S.priv) + threadIdx.x;
+        uint16_t* wc = reinterpret_cast<uint16_t*>(reinterpret_cast<long long*>(S.priv) + P1_WW * P1_T) + threadIdx.x;
+        wd[rel * P1_T] += kd;
+        wc[rel * P1_T] += 1;
+    } else if (hot) {
         // DOUBLE (emulate.py:133): fl(x*y) in units of 2^(e-52)
         const double scale = __hiloint2double((int)((3121u - esum) << 20), 0);   // 2^(52-e)
         const long long kd = __double2ll_rn(__dmul_rn(__dmul_rn(xv, yv), scale));
@@ -237,14 +249,27 @@ __device__ __forceinline__ void p1_enqueue(P1Shared& S, int64_t* __restrict__ A,
 
 // reduce the private slots into the CTA totals, push the cold table to the
 // global tables, clear both (all threads of the CTA)
-template <bool FULL>
+template <bool FULL, int WW = P1_W>
 __device__ __forceinline__ void p1_flush(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B, int tid) {
     __syncthreads();
     const int warp = tid >> 5, lane = tid & 31;
-    for (int r = warp; r < P1_W; r += P1_T / 32) {
+    for (int r = warp; r < WW; r += P1_T / 32) {
         uint64_t dlo = 0;
         int64_t dhi = 0;
         long long ss = 0, hs = 0, cs = 0;
+        if (WW == P1_WW) {
+            long long* wd = reinterpret_cast<long long*>(S.priv);
+            uint16_t* wc = reinterpret_cast<uint16_t*>(wd + P1_WW * P1_T);
+            for (int i = lane; i < P1_T; i += 32) {
+                const int64_t d = wd[r * P1_T + i];
+                wd[r * P1_T + i] = 0;
+                const uint64_t nl = dlo + (uint64_t)d;
+                dhi += (d >> 63) + (nl < dlo ? 1 : 0);
+                dlo = nl;
+                cs += wc[r * P1_T + i];
+                wc[r * P1_T + i] = 0;
+            }
+        } else
         for (int i = lane; i < P1_T; i += 32) {
             ulonglong2 v = S.priv[r * P1_T + i];
             S.priv[r * P1_T + i] = make_ulonglong2(0ull, 0ull);
@@ -333,7 +358,7 @@ __device__ __forceinline__ void p1_load(const double* __restrict__ x, const doub
     }
 }
 
-template <bool FULL, bool QUEUE, int V>
+template <bool FULL, bool QUEUE, int V, int WW = P1_W>
 __device__ __forceinline__ void p1_tile(P1Shared& S, ulonglong2* __restrict__ my, int kbias,
                                         int64_t* __restrict__ A, int64_t* __restrict__ B,
                                         const double (&xv)[2 * V], const double (&yv)[2 * V], int64_t e0,
@@ -341,7 +366,7 @@ __device__ __forceinline__ void p1_tile(P1Shared& S, ulonglong2* __restrict__ my
     if (fulltile) {
 #pragma unroll
         for (int j = 0; j < 2 * V; ++j) {
-            const bool c = p1_elem<FULL, QUEUE>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+            const bool c = p1_elem<FULL, QUEUE, WW>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
             if (QUEUE) p1_enqueue(S, A, B, tid >> 5, tid & 31, qn, c, xv[j], yv[j], zc, nf);
         }
     } else {
@@ -349,7 +374,7 @@ __device__ __forceinline__ void p1_tile(P1Shared& S, ulonglong2* __restrict__ my
         for (int j = 0; j < 2 * V; ++j) {
             bool c = false;
             if (e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1) < n)
-                c = p1_elem<FULL, QUEUE>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
+                c = p1_elem<FULL, QUEUE, WW>(S, my, kbias, A, B, xv[j], yv[j], zc, nf);
             if (QUEUE) p1_enqueue(S, A, B, tid >> 5, tid & 31, qn, c, xv[j], yv[j], zc, nf);
         }
     }
@@ -368,7 +393,7 @@ __device__ __forceinline__ void p1_prefetch_l2(const double* x, const double* y,
 // persistent loop over tiles.  PF: register double buffering (the loads of
 // the CTA's next tile are in flight while the current one is processed).
 // L2D > 0: one thread per CTA bulk-prefetches the tile L2D+1 iterations ahead into L2.
-template <bool NORM, bool VEC, bool FULL, bool QUEUE, int V, bool PF, int L2D>
+template <bool NORM, bool VEC, bool FULL, bool QUEUE, int V, bool PF, int L2D, int WW = P1_W>
 __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ x, const double* __restrict__ y,
                                         int64_t n, int64_t* __restrict__ A, int64_t* __restrict__ B, int tid,
                                         uint32_t* zc, uint32_t* nf) {
@@ -383,7 +408,7 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
     uint32_t qn = 0;                                   // warp queue fill (warp-uniform)
     auto flush = [&]() {
         if (QUEUE) p1_drain(S, A, B, tid >> 5, tid & 31, qn, zc, nf);
-        p1_flush<FULL>(S, A, B, tid);
+        p1_flush<FULL, WW>(S, A, B, tid);
     };
     if (!PF) {
         if (L2D > 0 && tid == 0) {   // warm the first prefetch window
@@ -394,7 +419,7 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
             bool f;
             if (L2D > 0 && tid == 0) p1_prefetch_l2<NORM>(x, y, n, t + (L2D + 1) * stride, TILE);
             p1_load<NORM, VEC, V>(x, y, n, t, tid, xv, yv, f);
-            p1_tile<FULL, QUEUE, V>(S, my, kbias, A, B, xv, yv, t * TILE, n, f, tid, qn, zc, nf);
+            p1_tile<FULL, QUEUE, V, WW>(S, my, kbias, A, B, xv, yv, t * TILE, n, f, tid, qn, zc, nf);
             if (++since == FLUSH) { flush(); since = 0; }
         }
     } else {
@@ -405,12 +430,12 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
         while (t < ntiles) {
             const int64_t tb = t + stride;
             if (tb < ntiles) p1_load<NORM, VEC, V>(x, y, n, tb, tid, xb, yb, fb);
-            p1_tile<FULL, QUEUE, V>(S, my, kbias, A, B, xa, ya, t * TILE, n, fa, tid, qn, zc, nf);
+            p1_tile<FULL, QUEUE, V, WW>(S, my, kbias, A, B, xa, ya, t * TILE, n, fa, tid, qn, zc, nf);
             if (++since == FLUSH) { flush(); since = 0; }
             if (tb >= ntiles) break;
             const int64_t ta = tb + stride;
             if (ta < ntiles) p1_load<NORM, VEC, V>(x, y, n, ta, tid, xa, ya, fa);
-            p1_tile<FULL, QUEUE, V>(S, my, kbias, A, B, xb, yb, tb * TILE, n, fb, tid, qn, zc, nf);
+            p1_tile<FULL, QUEUE, V, WW>(S, my, kbias, A, B, xb, yb, tb * TILE, n, fb, tid, qn, zc, nf);
             if (++since == FLUSH) { flush(); since = 0; }
             t = ta;
         }
@@ -461,6 +486,7 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
             cb = cb < 0 ? 0 : cb;
             S.cbase = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
             S.full = 1;
+            S.wide = 0;
             S.queue = 0;
             const bool slot_ok = blockIdx.x < (unsigned)LIST_SLOTS;
             S.list = prm.list + (int64_t)(slot_ok ? blockIdx.x : 0) * LIST_PER_SLOT;
@@ -528,29 +554,35 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
             }
         }
         __syncthreads();
-        {   // private window: argmax over starts b of pref[b+W] - pref[b], inside the safe range
-            unsigned long long best = 0ull;
+        {   // private window: argmax over starts b of pref[b+W] - pref[b], inside the safe
+            // range, for the 16-key window and the 24-key wide lean window
+            unsigned long long best = 0ull, best24 = 0ull;
             for (int b = P1_SAFE_LO + tid; b <= P1_SAFE_HI; b += P1_T) {
                 uint32_t s = pref[b + P1_W] - pref[b];
                 unsigned long long cand = ((unsigned long long)s << 32) | (uint32_t)(0xFFFFFFFFu - b);
                 best = cand > best ? cand : best;
+                if (b <= P1_SAFE_HI_W) {
+                    const uint32_t s24 = pref[b + P1_WW] - pref[b];
+                    const unsigned long long c24 = ((unsigned long long)s24 << 32) | (uint32_t)(0xFFFFFFFFu - b);
+                    best24 = c24 > best24 ? c24 : best24;
+                }
             }
             for (int o = 16; o; o >>= 1) {
                 unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
                 best = t > best ? t : best;
+                t = __shfl_xor_sync(0xffffffffu, best24, o);
+                best24 = t > best24 ? t : best24;
             }
             __syncthreads();
-            if ((tid & 31) == 0) S.red[tid >> 5] = best;
+            if ((tid & 31) == 0) { S.red[tid >> 5] = best; S.red[P1_T / 32 + (tid >> 5)] = best24; }
             __syncthreads();
             if (tid == 0) {
-                unsigned long long m = 0ull;
-                for (int w = 0; w < P1_T / 32; ++w) m = S.red[w] > m ? S.red[w] : m;
+                unsigned long long m = 0ull, m24 = 0ull;
+                for (int w = 0; w < P1_T / 32; ++w) {
+                    m = S.red[w] > m ? S.red[w] : m;
+                    m24 = S.red[P1_T / 32 + w] > m24 ? S.red[P1_T / 32 + w] : m24;
+                }
                 int b = (m >> 32) ? (int)(0xFFFFFFFFu - (uint32_t)m) : (KOFF - 8);   // default near e = 0
-                S.base = b;
-                int cb = b - (P1_CW - P1_W) / 2;
-                cb = cb < 0 ? 0 : cb;
-                cb = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
-                S.cbase = cb;
                 // lean / full decision (see header); only speed depends on it
                 int full = 0;
                 if (SMALL || (prm.mode & 3) == 2 || prm.input_mu != 52) full = 1;
@@ -567,13 +599,43 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                     }
                 }
                 S.full = full;
+                // wide lean window (24 keys): a lean CTA whose 16-key window misses more
+                // than 3% of its sample switches to the best 24-key window when that
+                // covers more and none of its keys can plausibly score below 27
+                int wide = 0, ww = P1_W;
+                if (!full && (m24 >> 32) && ((prm.mode & 16) || ((prm.mode & 3) == 0 && (prm.mode & 12) == 0))) {
+                    const uint32_t ns = pref[KEYS];
+                    const int b24 = (int)(0xFFFFFFFFu - (uint32_t)m24);
+                    const uint32_t cov16 = pref[b + P1_W] - pref[b], cov24 = pref[b24 + P1_WW] - pref[b24];
+                    bool ok = (prm.mode & 16) != 0;
+                    if (!ok && (uint64_t)cov16 * 100u < (uint64_t)ns * 97u && cov24 > cov16) {
+                        ok = true;
+                        const int fl = flexp_bits(dbits(prm.epsilon));
+                        for (int r = 0; r < P1_WW; ++r) {
+                            const uint32_t c = hist[b24 + r];
+                            if (!c) continue;
+                            const double mest = (double)c * (double)prm.n_total / (double)ns;
+                            const int lg = mest >= 1.0 ? flexp_bits(dbits(mest)) : 0;
+                            const int score = lg - 2 + (b24 + r - S.kmax) - fl + 1;
+                            if (score > -6 && score < 27) ok = false;
+                        }
+                    }
+                    if (ok) { wide = 1; ww = P1_WW; b = b24; }
+                }
+                S.wide = wide;
+                S.base = b;
+                int cb = b - (P1_CW - ww) / 2;
+                cb = cb < 0 ? 0 : cb;
+                cb = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
+                S.cbase = cb;
                 const bool slot_ok = blockIdx.x < (unsigned)LIST_SLOTS;
                 S.list = prm.list + (int64_t)(slot_ok ? blockIdx.x : 0) * LIST_PER_SLOT;
                 S.list_fill = slot_ok ? prm.list_fill[blockIdx.x] : (uint32_t)LIST_PER_SLOT;   // no slot: never write
                 S.collect = prm.collect;
                 // queue mode when more than 1/128 of the sample lies outside the private window
-                const uint32_t ns = pref[KEYS], cov = pref[b + P1_W] - pref[b];
-                S.queue = (prm.mode >> 2) == 1 ? 1 : ((prm.mode >> 2) == 2 ? 0 : ((ns - cov) * 128u > ns));
+                const uint32_t ns = pref[KEYS], cov = pref[b + ww] - pref[b];
+                const int qm = (prm.mode >> 2) & 3;
+                S.queue = qm == 1 ? 1 : (qm == 2 ? 0 : ((ns - cov) * 128u > ns));
             }
         }
         __syncthreads();
@@ -584,7 +646,7 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         S.c_cnt[k] = 0u; S.c_d0[k] = 0u; S.c_d1[k] = 0u; S.c_d2[k] = 0u; S.c_d3[k] = 0u;
         S.c_s0[k] = 0u; S.c_s1[k] = 0u; S.c_h[k] = 0u;
     }
-    if (tid < P1_W) { S.t_d[tid] = 0; S.t_s[tid] = 0; S.t_h[tid] = 0; S.t_c[tid] = 0; }
+    if (tid < P1_WW) { S.t_d[tid] = 0; S.t_s[tid] = 0; S.t_h[tid] = 0; S.t_c[tid] = 0; }
     __syncthreads();
 
     // ---- main streaming loop (persistent grid over tiles)
@@ -592,6 +654,9 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     const bool fullmode = SMALL || S.full != 0;
     if (SMALL) {
         p1_main<NORM, VEC, true, false, V, false, 0>(S, x, y, n, A, B, tid, &zc, &nf);
+    } else if (S.wide) {
+        if (S.queue) p1_main<NORM, VEC, false, true, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
+        else p1_main<NORM, VEC, false, false, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
     } else if (S.queue) {
         if (fullmode) p1_main<NORM, VEC, true, true, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
         else p1_main<NORM, VEC, false, true, V, PF, L2D>(S, x, y, n, A, B, tid, &zc, &nf);
@@ -601,7 +666,7 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     }
 
     // ---- publish CTA partials (the cold table was pushed by the last flush)
-    for (int r = tid; r < P1_W; r += P1_T) {
+    for (int r = tid; r < (S.wide ? P1_WW : P1_W); r += P1_T) {
         if (S.t_c[r]) {
             push_key(A, B, S.base + r, (unsigned long long)S.t_c[r], S.t_d[r], S.t_s[r], S.t_h[r]);
             atomicAdd(reinterpret_cast<unsigned long long*>(A + A_PRIV + S.base + r), (unsigned long long)S.t_c[r]);
