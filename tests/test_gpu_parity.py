@@ -358,3 +358,21 @@ def test_c_abi_dot_host(n, norm):
         assert res.value == rep.value and res.n_bins == len(rep.params.bins)
         assert [(bins[i].lower, bins[i].upper, bins[i].cardinality) for i in range(res.n_bins)] == \
                [(b.lower, b.upper, b.cardinality) for b in rep.params.bins]
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 255, 4096, 100003])
+def test_graph_one_call_path_small(n):
+    # run_device(timing=False) -> qdot_b200_dot: the cached-graph pipeline with
+    # the host-mapped result; repeated calls (graph replay) stay identical
+    from paper_2105_00115_b200.kernel import run_device
+    rng = np.random.default_rng(1000 + n)
+    x = rng.standard_normal(n) * np.exp2(rng.integers(-20, 20, n))
+    y = rng.standard_normal(n)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    cfg = Q.ToleranceConfig(1e-6, Q.SplitMode.PER_BIN)
+    ref = O.qdot(x, y, 1e-6, "per-bin", 52, "exact")
+    for _ in range(3):
+        res, bins, _ = run_device(xd, yd, n, False, cfg, Q.ExactBinning(), timing=False)
+        assert res.status == 0 and res.n_bins == ref.n_bins
+        assert res.value == ref.value or (n == 0 and res.value == 0.0)
+        assert [bins[i].cardinality for i in range(res.n_bins)] == [b.cardinality for b in ref.bins]
