@@ -386,8 +386,10 @@ def main():
     peak, peak_kind = measured_peak()
     bytes_per_elem = 8 if args.norm else 16
     achieved = n * bytes_per_elem / (p1_ms * 1e-3) / 1e9
-    traffic, traffic_n = profile_traffic()
-    if traffic is not None and traffic_n and traffic_n != n:
+    traffic, traffic_n = profile_traffic()          # committed ncu capture of the C2 (x != y) launch
+    if args.norm:
+        traffic = None
+    elif traffic is not None and traffic_n and traffic_n != n:
         traffic = traffic * n / traffic_n
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": "qd::k_pass1",
