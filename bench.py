@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU")
+    ap.add_argument("--elements", "--n", dest="n", type=int, default=N_PER_GPU, help="elements per GPU")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample", type=int, default=1 << 24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -261,11 +261,19 @@ def main():
         return
     import torch
     import ctypes
+    # QDOT_BENCH_TEST_SHARED_GPU=1: every rank on cuda:0 over gloo -- exercises the
+    # multi-rank path (exchange, max-over-ranks timing, sharded e2e) on a one-GPU
+    # box; its timings mean nothing
+    shared = os.environ.get("QDOT_BENCH_TEST_SHARED_GPU") == "1"
+    local = 0 if shared else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2105_00115_b200 as Q
     from paper_2105_00115_b200 import _lib
     from paper_2105_00115_b200.device import config_struct, thread_state
