@@ -217,7 +217,53 @@ def measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, norm, Q, config_
                          "kernel": "qd::k_batched", "ms": bms, "dots_per_s": R / (bms * 1e-3),
                          "elements_per_s": R * L / (bms * 1e-3),
                          "GBps": R * L * 16 / (bms * 1e-3) / 1e9, "general_rows": general}
-    del X, Y
+    del X, Y, vals, cnt, info
+    torch.cuda.empty_cache()
+
+    # BASELINE configs[2] (C3): the ill-conditioned distribution of SURVEY.md §8d
+    # (cond ~1e12, exponent sums spanning +-300), generated on the device with
+    # torch (same law as oracle.gen_illcond, other bits), eps 1e-12, whole step
+    h = n // 2
+
+    def drops():
+        d = torch.floor(torch.empty(h, device=dev, dtype=torch.float64).exponential_(0.25, generator=g)).clamp_(max=300)
+        m = torch.rand(h, device=dev, generator=g) < 1e-3
+        d[m] = torch.randint(0, 301, (int(m.sum()),), device=dev, generator=g).double()
+        return d
+
+    a, b = drops(), drops()
+    sgn = torch.where(torch.rand(h, device=dev, generator=g) < 0.5, -1.0, 1.0).double()
+    x1 = sgn * torch.ldexp(torch.rand(h, device=dev, generator=g, dtype=torch.float64) * 0.5 + 0.5, 150 - a)
+    y1 = torch.ldexp(torch.rand(h, device=dev, generator=g, dtype=torch.float64) * 0.5 + 0.5, 150 - b)
+    delta = (torch.rand(h, device=dev, generator=g, dtype=torch.float64) * 2 - 1) * 2.0 ** -25
+    perm = torch.randperm(2 * h, device=dev, generator=g)
+    xc = torch.cat([x1, x1])[perm].contiguous()
+    yc = torch.cat([y1, -y1 * (1.0 + delta)])[perm].contiguous()
+    del a, b, sgn, x1, y1, delta, perm
+    c3 = config_struct(Q.ToleranceConfig(1e-12), Q.ExactBinning())
+    from paper_2105_00115_b200.device import thread_state
+    st = thread_state(dev)
+    ws = st.ws_ptr
+    m = 2 * h
+
+    def c3_step():
+        _lib.check(lib.qdot_b200_begin(ws, s), lib)
+        _lib.check(lib.qdot_b200_pass1(xc.data_ptr(), yc.data_ptr(), m, 0, ctypes.byref(c3), m, ws, s), lib)
+        _lib.check(lib.qdot_b200_score_finalize(ws, m, ctypes.byref(c3), s), lib)
+        _lib.check(lib.qdot_b200_pass2(xc.data_ptr(), yc.data_ptr(), m, 0, ws, s), lib)
+        _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+    for _ in range(3):
+        c3_step()
+    e0.record(stream)
+    for _ in range(reps):
+        c3_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    cms = e0.elapsed_time(e1) / reps
+    res["illcond_c3"] = {"workload": "BASELINE configs[2]: n=2^28 ill-conditioned (SURVEY.md 8d law, device-generated), "
+                                     "eps 1e-12, exact, whole qdot step",
+                         "ms": cms, "elements_per_s": m / (cms * 1e-3), "GBps": m * 16 / (cms * 1e-3) / 1e9}
+    del xc, yc
     torch.cuda.empty_cache()
     return res
 
