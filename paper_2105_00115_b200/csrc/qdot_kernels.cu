@@ -690,6 +690,7 @@ static cudaError_t launch_pass1_t(const double* x, const double* y, int64_t n, i
     return cudaGetLastError();
 }
 
+#ifdef QDOT_B200_P1_TUNING
 // pass-1 variant (vector width / prefetch); QDOT_B200_P1_VARIANT overrides for tuning
 static int p1_variant() {
     static int v = -1;
@@ -699,6 +700,7 @@ static int p1_variant() {
     }
     return v;
 }
+#endif
 
 template <bool NORM, bool VEC>
 static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
@@ -706,14 +708,19 @@ static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, i
     // short inputs (at most two tiles per SM): the compact variant
     if ((prm.mode >> 2) == 0 && (prm.mode & 3) == 0 && n <= (int64_t)sm_count_cached() * 2 * (P1_T * 8))
         return launch_pass1_t<NORM, VEC, 4, false, 0, true>(x, y, n, A, B, prm, st);
+#ifdef QDOT_B200_P1_TUNING
+    // tuning builds only (-DQDOT_B200_P1_TUNING): alternative pass-1 shapes
     switch (p1_variant()) {
         case 1: return launch_pass1_t<NORM, VEC, 4, false, 0>(x, y, n, A, B, prm, st);   // no L2 prefetch
         case 2: return launch_pass1_t<NORM, VEC, 2, false, 3>(x, y, n, A, B, prm, st);
         case 3: return launch_pass1_t<NORM, VEC, 4, false, 2>(x, y, n, A, B, prm, st);
         case 4: return launch_pass1_t<NORM, VEC, 2, true, 0>(x, y, n, A, B, prm, st);    // register double buffer
-        default: return launch_pass1_t<NORM, VEC, 4, false, 3>(x, y, n, A, B, prm, st);  // tuned on B200
-                                                         // (norm mode: V=8 measured slower)
+        default: break;
     }
+#endif
+    // V = 4 double2 per thread per tile, bulk L2 prefetch 4 tiles ahead: tuned on
+    // B200 (norm mode: V = 8 measured slower)
+    return launch_pass1_t<NORM, VEC, 4, false, 3>(x, y, n, A, B, prm, st);
 }
 
 cudaError_t launch_pass1(const double* x, const double* y, int64_t n, bool norm, int64_t* A, int64_t* B,

@@ -1,4 +1,5 @@
 #!/bin/bash
+# needs a tuning build: NVCC extra flag -DQDOT_B200_P1_TUNING (variants are not in the default library)
 mkdir -p gpurun_out
 OUT=gpurun_out/p1_sweep_${1:-x}.jsonl
 : > $OUT
