@@ -97,7 +97,9 @@ typedef struct {
     int32_t early_terminated;
     int32_t pass2_needed;    /* a second streaming pass was required              */
     int32_t half_order_sensitive; /* any bin with flags bit0                      */
-    int32_t reserved[5];
+    int32_t select_ns;       /* device time: pass 1 start -> scoring done         */
+    int32_t compute_ns;      /* device time: scoring done -> finalize done        */
+    int32_t reserved[3];
 } qdot_result;
 
 /* Workspace regions, in bytes from the start of ws.  Region A (int64[a_len],

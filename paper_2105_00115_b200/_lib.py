@@ -38,7 +38,7 @@ class QdotResult(ctypes.Structure):
                 ("status", ctypes.c_int32), ("n_bins", ctypes.c_int32), ("e_min", ctypes.c_int32),
                 ("e_max", ctypes.c_int32), ("early_terminated", ctypes.c_int32),
                 ("pass2_needed", ctypes.c_int32), ("half_order_sensitive", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("select_ns", ctypes.c_int32), ("compute_ns", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 class QdotExactResult(ctypes.Structure):

@@ -95,13 +95,28 @@ constexpr int64_t OFF_A = 0;
 constexpr int64_t OFF_B = OFF_A + BYTES_A;
 constexpr int64_t OFF_LOCAL = OFF_B + BYTES_B;                   // rank-local counters (zeroed by begin)
 constexpr int64_t LIST_SLOTS = 1024;                             // one list slot per pass-1 CTA index
-constexpr int64_t BYTES_LOCAL = LIST_SLOTS * 4;                  // uint32 fill per slot
+constexpr int64_t BYTES_LOCAL = LIST_SLOTS * 4 + 64;             // uint32 fill per slot, then phase stamps
 constexpr int64_t OFF_LUT_BIN = OFF_LOCAL + BYTES_LOCAL;         // int32[KEYS]
 constexpr int64_t OFF_LUT_P2 = OFF_LUT_BIN + 4224 * 4;           // uint32[KEYS]
 constexpr int64_t OFF_META = OFF_LUT_P2 + 4224 * 4;              // ScoreMeta
 constexpr int64_t OFF_RESULT = OFF_META + 256;                   // qdot_result
 constexpr int64_t OFF_BINS = OFF_RESULT + 256;                   // qdot_bin[KEYS + 1]
 constexpr int64_t BYTES_BINS = (int64_t)sizeof(qdot_bin) * (KEYS + 1);
+#ifdef __CUDACC__
+// device timestamps of the phases (ns, %globaltimer) in the rank-local area,
+// located from the region-A pointer every kernel receives: [0] pass 1 start,
+// [1] score done (select = [1]-[0]), finalize end - [1] = compute
+__device__ __forceinline__ unsigned long long* ws_stamps(const int64_t* A) {
+    return reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(const_cast<int64_t*>(A)) - OFF_A + OFF_LOCAL + LIST_SLOTS * 4);
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 // cold-element list: (x, y) of every element pass 1 did not accumulate in a
 // private window, so that pass 2 (when it is needed only for such keys) reads
 // this list instead of streaming both vectors again

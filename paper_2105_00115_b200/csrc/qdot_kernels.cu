@@ -355,6 +355,7 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         sm = m;
         *meta = m;
     }
+    if (tid == 0) ws_stamps(A)[1] = global_ns();             // parameter selection done
     __syncthreads();
     // no pass 2 needed (the common case): finalize here and save a launch;
     // k_finalize then exits on meta->done
@@ -620,6 +621,11 @@ __device__ void finalize_body(const int64_t* __restrict__ A, const int64_t* __re
         r.early_terminated = m.early;
         r.pass2_needed = m.need_p2;
         r.half_order_sensitive = s_half;
+        const unsigned long long* ts = ws_stamps(A);
+        const unsigned long long now = global_ns();
+        const unsigned long long sel = ts[1] > ts[0] ? ts[1] - ts[0] : 0ull, cmp = now > ts[1] ? now - ts[1] : 0ull;
+        r.select_ns = (int32_t)(sel < 0x7FFFFFFFull ? sel : 0x7FFFFFFFull);
+        r.compute_ns = (int32_t)(cmp < 0x7FFFFFFFull ? cmp : 0x7FFFFFFFull);
         *res = r;
     }
 }

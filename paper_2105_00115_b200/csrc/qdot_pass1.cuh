@@ -455,6 +455,7 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     const int tid = threadIdx.x;
     constexpr int TILE = P1_T * 2 * V;
     const int64_t ntiles = (n + TILE - 1) / TILE;
+    if (blockIdx.x == 0 && tid == 0) atomicCAS(ws_stamps(A), 0ull, global_ns());   // first launch only
 
     if (SMALL) {
         // short inputs: the window only has to be reasonable -- [kmax - W + 3,

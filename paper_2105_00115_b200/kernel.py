@@ -28,8 +28,7 @@ from . import _lib
 from .binning import Bin, ExactBinning, Strategy, strategy_label
 from .device import as_device_vector, config_struct, require_cuda, stream_handle, thread_state
 from .exact import ReferenceResult, reference_dot  # noqa: F401  (kernel.py:75-133 live here in the reference)
-from .scoring import (ParameterSet, PrecisionLevel, SplitMode, ToleranceConfig, absolute_bound_term,
-                      relative_bound_term)
+from .scoring import ParameterSet, PrecisionLevel, SplitMode, ToleranceConfig
 
 __all__ = ["QdotReport", "qdot", "select_parameters", "run_device", "ReferenceResult", "reference_dot"]
 
@@ -111,7 +110,8 @@ def run_device(xd, yd, n: int, norm: bool, cfg: ToleranceConfig, strategy, st=No
         # to host-mapped memory (qdot_b200_dot)
         _lib.check(lib.qdot_b200_dot(xp, yp, n, int(norm), ctypes.byref(c), ws, ctypes.byref(st.result), st.bins,
                                      _lib.KEYS + 1, s), lib)
-        return st.result, st.bins, {"select": 0, "compute": 0, "reference": 0}
+        res = st.result
+        return res, st.bins, {"select": int(res.select_ns), "compute": int(res.compute_ns), "reference": 0}
     torch_stream = None
     if timing:
         import torch
@@ -135,23 +135,55 @@ def run_device(xd, yd, n: int, norm: bool, cfg: ToleranceConfig, strategy, st=No
     return st.result, st.bins, phase
 
 
-def _build_params(res, cbins, cfg, strategy, indexer) -> ParameterSet:
-    ps = ParameterSet(bins=[], e_min=int(res.e_min), e_max=int(res.e_max), strategy=strategy, tolerance=cfg,
+_BIN_DTYPE = np.dtype([("lower", "<i8"), ("upper", "<i8"), ("cardinality", "<i8"), ("score", "<i8"),
+                       ("precision", "<i4"), ("first_key", "<i4"), ("last_key", "<i4"), ("flags", "<i4"),
+                       ("value", "<f8")])
+assert _BIN_DTYPE.itemsize == ctypes.sizeof(_lib.QdotBin)
+_EPS_OF_CODE = np.array([PrecisionLevel.from_code(c).eps for c in range(4)])
+
+
+def _bin_rows(cbins, n_bins: int) -> np.ndarray:
+    """A private copy of the first n_bins device bin records (the ctypes table is
+    reused by the next call on this thread)."""
+    if n_bins <= 0:
+        return np.zeros(0, dtype=_BIN_DTYPE)
+    return np.frombuffer(cbins, dtype=_BIN_DTYPE, count=n_bins).copy()
+
+
+def _bound_terms(rows: np.ndarray, shift: int) -> np.ndarray:
+    """M * ldexp(eps, upper - shift + 1) per bin, rounded exactly like the
+    scalar terms of scoring.py:171-178 (ldexp first, then the product).  An
+    overflowing ldexp falls back to math.ldexp, which raises OverflowError
+    like the reference."""
+    eps = _EPS_OF_CODE[rows["precision"]]
+    k = rows["upper"] - shift + 1
+    with np.errstate(over="ignore"):
+        p2 = np.ldexp(eps, np.clip(k, -4000, 4000))
+    if not np.all(np.isfinite(p2)):
+        p2 = np.array([math.ldexp(float(e), int(kk)) for e, kk in zip(eps, k)])
+    return rows["cardinality"].astype(np.float64) * p2
+
+
+def _make_bin_objects(rows: np.ndarray, indexer):
+    def make(ps):
+        return [Bin(lower=int(r["lower"]), upper=int(r["upper"]), cardinality=int(r["cardinality"]),
+                    score=int(r["score"]), precision=PrecisionLevel.from_code(int(r["precision"])),
+                    value=float(r["value"]), flags=int(r["flags"]), first_key=int(r["first_key"]),
+                    last_key=int(r["last_key"]), indexer=indexer, owner=ps) for r in rows]
+    return make
+
+
+def _build_params(res, cbins, cfg, strategy, indexer, rows=None) -> ParameterSet:
+    if rows is None:
+        rows = _bin_rows(cbins, int(res.n_bins))
+    ps = ParameterSet(bins=None, e_min=int(res.e_min), e_max=int(res.e_max), strategy=strategy, tolerance=cfg,
                       early_terminated=bool(res.early_terminated), n=int(res.n), eps_eff=float(res.eps_eff),
-                      n_bins=int(res.n_bins), zero_count=int(res.zero_count), _indexer=indexer)
-    bins = []
-    for i in range(res.n_bins):
-        cb = cbins[i]
-        bins.append(Bin(lower=int(cb.lower), upper=int(cb.upper), cardinality=int(cb.cardinality),
-                        score=int(cb.score), precision=PrecisionLevel.from_code(cb.precision),
-                        value=float(cb.value), flags=int(cb.flags), first_key=int(cb.first_key),
-                        last_key=int(cb.last_key), indexer=indexer, owner=ps))
-    ps.bins = bins
-    # ParameterSet.rel_bound: plain left-to-right sum (scoring.py:195-199)
-    rb = 0.0
-    for b in bins:
-        rb += relative_bound_term(b, ps.e_max)
-    ps.rel_bound = rb
+                      n_bins=int(res.n_bins), zero_count=int(res.zero_count), _indexer=indexer,
+                      _make_bins=_make_bin_objects(rows, indexer))
+    # ParameterSet.rel_bound: plain left-to-right sum from 0.0 (scoring.py:195-199);
+    # np.add.accumulate is sequential, and the terms are >= 0
+    rel = _bound_terms(rows, int(res.e_max))
+    ps.rel_bound = float(np.add.accumulate(rel)[-1]) if rel.size else 0.0
     return ps
 
 
@@ -198,9 +230,10 @@ def _raise_status(res) -> None:
 
 def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer) -> QdotReport:
     """Host-side report assembly (kernel.py:205-240)."""
-    params = _build_params(res, cbins, cfg, strategy, indexer)
-    abs_bound = math.fsum(absolute_bound_term(b) for b in params.bins)
-    rel_bound = math.fsum(relative_bound_term(b, params.e_max) for b in params.bins)
+    rows = _bin_rows(cbins, int(res.n_bins))
+    params = _build_params(res, cbins, cfg, strategy, indexer, rows)
+    abs_bound = math.fsum(_bound_terms(rows, 0).tolist())
+    rel_bound = math.fsum(_bound_terms(rows, params.e_max).tolist())
     rel_hypothesis = "assumed"
     rel_bound_e = None
     if is_norm:
@@ -210,10 +243,9 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
         if fe is None:
             rel_hypothesis = "violated" if not is_norm else rel_hypothesis
         else:
-            holds = params.e_max <= fe or not params.bins
+            holds = params.e_max <= fe or rows.size == 0
             rel_hypothesis = "holds" if (holds or is_norm) else "violated"
-            rel_bound_e = math.fsum(b.cardinality * math.ldexp(b.precision.eps, b.upper - fe + 1)
-                                    for b in params.bins)
+            rel_bound_e = math.fsum(_bound_terms(rows, int(fe)).tolist())
     counts = {level: 0 for level in PrecisionLevel}
     for i, level in enumerate((PrecisionLevel.PERFORATE, PrecisionLevel.HALF, PrecisionLevel.SINGLE,
                                PrecisionLevel.DOUBLE)):
@@ -294,18 +326,15 @@ def _run_host_pipelined(xh, yh, norm: bool, cfg: ToleranceConfig, strategy):
     comp = torch.cuda.current_stream(device)
     s = comp.cuda_stream
     ws = st.ws_ptr
-    st.ev[0].record(comp)
     _lib.check(lib.qdot_b200_begin(ws, s), lib)
     xd, yd = h2d_pass1(xh, yh, norm, c, n, st, device)
     _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), s), lib)
-    st.ev[1].record(comp)
     _lib.check(lib.qdot_b200_pass2(xd.data_ptr(), yd.data_ptr(), n, int(norm), ws, s), lib)
     _lib.check(lib.qdot_b200_finalize(ws, s), lib)
-    st.ev[2].record(comp)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
-    phase = {"select": int(st.ev[0].elapsed_time(st.ev[1]) * 1e6),
-             "compute": int(st.ev[1].elapsed_time(st.ev[2]) * 1e6), "reference": 0}
-    return st.result, st.bins, phase, xd, yd
+    res = st.result
+    phase = {"select": int(res.select_ns), "compute": int(res.compute_ns), "reference": 0}
+    return res, st.bins, phase, xd, yd
 
 
 def qdot(x, y, cfg: ToleranceConfig, strategy: Strategy = None, reference=None) -> QdotReport:
@@ -333,7 +362,9 @@ def qdot(x, y, cfg: ToleranceConfig, strategy: Strategy = None, reference=None) 
             return report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer)
     is_norm, xd, yd = _prepare(x, y)
     n = int(xd.shape[0])
-    res, cbins, phase = run_device(xd, yd, n, is_norm, cfg, strategy)
+    # one C call (cached CUDA graph, host-mapped result); phase_ns comes from
+    # device timestamps (select: pass 1 + scoring, compute: pass 2 + finalize)
+    res, cbins, phase = run_device(xd, yd, n, is_norm, cfg, strategy, timing=False)
     _raise_status(res)
     indexer = _Indexer(xd, yd, n, is_norm, xd.device)
     return report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer)

@@ -175,6 +175,21 @@ class ParameterSet:
     zero_count: int = 0
     _indexer: Optional[object] = field(default=None, repr=False)
     _zero_idx: Optional[np.ndarray] = field(default=None, repr=False)
+    # bins=None with a _make_bins factory: the Bin objects are built on first
+    # access (most callers only read the report's value, counts and bounds)
+    _make_bins: Optional[object] = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        if self.bins is None and self._make_bins is not None:
+            del self.bins                       # resolved by __getattr__ on first read
+
+    def __getattr__(self, name):
+        if name == "bins":
+            make = self.__dict__.get("_make_bins")
+            value = make(self) if make is not None else []
+            self.__dict__["bins"] = value
+            return value
+        raise AttributeError(name)
 
     @property
     def zero_idx(self) -> np.ndarray:
