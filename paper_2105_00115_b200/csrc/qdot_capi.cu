@@ -233,10 +233,12 @@ struct FastState {
     cudaStream_t cap = nullptr;
     struct Entry { GraphKey k; cudaGraphExec_t exec; uint64_t use; };
     std::vector<Entry> cache;
+    std::vector<GraphKey> seen;   // keys met once: a graph is captured on the second call only
     uint64_t tick = 0;
     void clear() {
         for (auto& e : cache) cudaGraphExecDestroy(e.exec);
         cache.clear();
+        seen.clear();
         if (cap) cudaStreamDestroy(cap);
         if (dev_seq) cudaFree(dev_seq);
         if (host) cudaFreeHost(host);
@@ -279,6 +281,15 @@ cudaGraphExec_t graph_for(const GraphKey& k, const qdot_config* cfg) {
     FastState& F = g_fast;
     for (auto& e : F.cache)
         if (e.k == k) { e.use = ++F.tick; return e.exec; }
+    // a capture costs more than a few eager launches: only repeated calls get one
+    bool repeat = false;
+    for (auto& sk : F.seen)
+        if (sk == k) { repeat = true; break; }
+    if (!repeat) {
+        if (F.seen.size() >= 64) F.seen.erase(F.seen.begin());
+        F.seen.push_back(k);
+        return nullptr;
+    }
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(F.cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return nullptr;
     int r = enqueue_dot(k.x, k.y, k.n, k.norm, cfg, k.ws, F.cap);
@@ -294,6 +305,8 @@ cudaGraphExec_t graph_for(const GraphKey& k, const qdot_config* cfg) {
         cudaGraphExecDestroy(F.cache[old].exec);
         F.cache.erase(F.cache.begin() + old);
     }
+    for (size_t i = 0; i < F.seen.size(); ++i)
+        if (F.seen[i] == k) { F.seen.erase(F.seen.begin() + i); break; }
     F.cache.push_back({k, exec, ++F.tick});
     return exec;
 }
@@ -343,7 +356,7 @@ int qdot_b200_dot(const double* x, const double* y, int64_t n, int norm, const q
     cudaGraphExec_t exec = graph_for(k, cfg);
     if (exec) {
         QD_CHECK(cudaGraphLaunch(exec, st), "graph launch");
-    } else if ((v = enqueue_dot(x, norm ? x : y, n, norm, cfg, ws, st))) {   // capture refused: same sequence, eagerly
+    } else if ((v = enqueue_dot(x, norm ? x : y, n, norm, cfg, ws, st))) {   // first call / no capture: eagerly
         return v;
     }
     return collect(st, ws, out, bins, max_bins);
