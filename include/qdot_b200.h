@@ -197,6 +197,12 @@ int qdot_b200_bin_ids(const double* x, const double* y, int64_t n, int norm, con
  * are only read through the row extents (may be NULL for an empty matrix). */
 int qdot_b200_csr_spmv(int64_t n_rows, const int64_t* indptr, const void* indices, int index_bytes,
                        const double* data, const double* x, double* y, void* stream);
+/* the same product from a sliced-ELL copy of the matrix (slices of 32 rows;
+ * entry j of row r at slice_off[r / 32] + 32 j + r % 32; row_len[r] entries;
+ * int32 column indices): coalesced loads, identical per-row summation order,
+ * hence identical results. */
+int qdot_b200_sell_spmv(int64_t n_rows, const int64_t* slice_off, const int32_t* row_len, const int32_t* cols,
+                        const double* vals, const double* x, double* y, void* stream);
 /* elementwise vector updates of the solvers (apps.py:216-220, 306-308), each
  * bit-identical to the numpy expression: op 0 out = a + s*b, op 1 out = a - s*b
  * (s*b rounded first), op 2 out = a / s (b unused).  out may alias a or b. */

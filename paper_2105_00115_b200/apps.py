@@ -124,6 +124,7 @@ class SparseMatrix:
     symmetric: bool = True
     _csr: Optional[sp.csr_matrix] = field(default=None, repr=False, compare=False)
     _device: Optional[tuple] = field(default=None, repr=False, compare=False)
+    _sell: Optional[object] = field(default=None, repr=False, compare=False)
 
     @classmethod
     def from_csr(cls, m: sp.csr_matrix, symmetric: bool = True) -> "SparseMatrix":
@@ -148,13 +149,53 @@ class SparseMatrix:
             self._device = (indptr, indices, int(idx.dtype.itemsize), data)
         return self._device
 
+    def sell_arrays(self):
+        """Sliced-ELL copy (slices of 32 rows, column-major inside a slice),
+        built on the device from the CSR arrays; None when a column index does
+        not fit int32 or the padding would more than double the storage."""
+        if self._sell is None:
+            torch, device = _dev()
+            indptr, indices, _, data = self.device_arrays()
+            n = self.n
+            if n == 0 or self.indices.size == 0 or self.n > (1 << 31) - 1:
+                self._sell = False
+                return None
+            row_len = (indptr[1:] - indptr[:-1]).to(torch.int32)
+            ns = (n + 31) // 32
+            padded = torch.zeros(ns * 32, dtype=torch.int32, device=device)
+            padded[:n] = row_len
+            width = padded.view(ns, 32).max(dim=1).values.to(torch.int64)
+            slice_off = torch.zeros(ns + 1, dtype=torch.int64, device=device)
+            slice_off[1:] = torch.cumsum(width * 32, 0)
+            total = int(slice_off[-1])
+            if total > 2 * int(indptr[-1]) + 32 * ns:
+                self._sell = False
+                return None
+            rows = torch.repeat_interleave(torch.arange(n, device=device), row_len.to(torch.int64))
+            j = torch.arange(rows.numel(), device=device) - indptr[rows]
+            dest = slice_off[rows // 32] + 32 * j + rows % 32
+            cols = torch.zeros(total, dtype=torch.int32, device=device)
+            vals = torch.zeros(total, dtype=torch.float64, device=device)
+            cols[dest] = indices.to(torch.int32)
+            vals[dest] = data
+            self._sell = (slice_off[:-1].contiguous(), row_len.contiguous(), cols, vals)
+        return self._sell or None
+
     def matvec_device(self, xd, out=None):
-        """y = A x with device vectors (qdot_b200_csr_spmv)."""
+        """y = A x with device vectors: sliced-ELL kernel when available, else
+        the CSR kernel (both sum each row like scipy's csr_matvec)."""
         torch, _ = _dev()
-        indptr, indices, ib, data = self.device_arrays()
         if out is None:
             out = torch.empty(self.n, dtype=torch.float64, device=xd.device)
         lib = _lib.load()
+        sell = self.sell_arrays()
+        if sell is not None:
+            so, rl, cols, vals = sell
+            _lib.check(lib.qdot_b200_sell_spmv(self.n, so.data_ptr(), rl.data_ptr(), cols.data_ptr(),
+                                               vals.data_ptr(), xd.data_ptr(), out.data_ptr(),
+                                               stream_handle(xd.device)), lib)
+            return out
+        indptr, indices, ib, data = self.device_arrays()
         _lib.check(lib.qdot_b200_csr_spmv(self.n, indptr.data_ptr(), indices.data_ptr(), ib, data.data_ptr(),
                                           xd.data_ptr(), out.data_ptr(), stream_handle(xd.device)), lib)
         return out
@@ -488,6 +529,7 @@ def apm(a: SparseMatrix, x0, tau: float = 1e-6, epsilon: float = 1e-7, split: Sp
             return body
 
         a.device_arrays()                                   # host->device copies cannot be captured
+        a.sell_arrays()
         graphs = [G.capture(body_for(bufs[0], bufs[1])), G.capture(body_for(bufs[1], bufs[0]))]
         while k < max_iters:
             r_zz, r_lam, _st = G.run(graphs[k % 2])

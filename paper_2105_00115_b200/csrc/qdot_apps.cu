@@ -53,6 +53,26 @@ __global__ void __launch_bounds__(T) k_csr_spmv(int64_t n_rows, const int64_t* _
     }
 }
 
+// sliced ELL (slices of 32 rows; entry j of row r at slice_off[r/32] + 32 j + r%32):
+// the 32 threads of a warp read consecutive values and column indices for
+// the same j -- coalesced -- while every row keeps scipy's sequential
+// left-to-right sum (padding is never read: each row stops at its length)
+__global__ void __launch_bounds__(T) k_sell_spmv(int64_t n_rows, const int64_t* __restrict__ slice_off,
+                                                 const int32_t* __restrict__ row_len,
+                                                 const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                                                 const double* __restrict__ x, double* __restrict__ y) {
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n_rows; i += (int64_t)gridDim.x * T) {
+        const int64_t base = __ldg(slice_off + (i >> 5)) + (i & 31);
+        const int len = __ldg(row_len + i);
+        double s = 0.0;
+        for (int j = 0; j < len; ++j) {
+            const int64_t k = base + 32 * (int64_t)j;
+            s = __dadd_rn(s, __dmul_rn(__ldg(vals + k), __ldg(x + __ldg(cols + k))));
+        }
+        y[i] = s;
+    }
+}
+
 // op 0: out = a + s*b; 1: out = a - s*b; 2: out = a / s.  out may alias a or b
 // (each element is read and written by the same thread), so no __restrict__.
 template <int OP>
@@ -216,6 +236,17 @@ int qdot_b200_csr_spmv(int64_t n_rows, const int64_t* indptr, const void* indice
         k_csr_spmv<int64_t><<<g, T, 0, st>>>(n_rows, indptr, static_cast<const int64_t*>(indices), data, x, y);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "csr_spmv");
+}
+
+int qdot_b200_sell_spmv(int64_t n_rows, const int64_t* slice_off, const int32_t* row_len, const int32_t* cols,
+                        const double* vals, const double* x, double* y, void* stream) {
+    if (n_rows < 0) return QDOT_ERR_ARG;
+    if (n_rows == 0) return QDOT_OK;
+    if (!slice_off || !row_len || !y) return QDOT_ERR_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_sell_spmv<<<grid_for(n_rows, 1), T, 0, st>>>(n_rows, slice_off, row_len, cols, vals, x, y);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "sell_spmv");
 }
 
 int qdot_b200_vec_update(int64_t n, int op, const double* a, double s, const double* b, double* out,

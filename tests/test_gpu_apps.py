@@ -107,6 +107,33 @@ def test_spmv_bitwise_scipy(shape, density, seed):
     assert a64.matvec(v).tobytes() == (m @ v).tobytes()
 
 
+def _ragged_csr(n, lens, seed):
+    rng = np.random.default_rng(seed)
+    indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    indices = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int32)
+    data = rng.standard_normal(indptr[-1]) * np.exp2(rng.integers(-30, 30, indptr[-1]))
+    return sp.csr_matrix((data, indices, indptr), shape=(n, n))
+
+
+@pytest.mark.parametrize("kind", ["ragged", "skewed", "tail"])
+def test_spmv_sliced_ell_vs_csr(kind):
+    """The sliced-ELL kernel (used when padding stays under 2x) and the CSR
+    kernel (the fallback) both equal scipy bit for bit on ragged rows, empty
+    rows and a row count that is not a multiple of the 32-row slice."""
+    rng = np.random.default_rng(11)
+    n = {"ragged": 1037, "skewed": 2000, "tail": 33}[kind]
+    lens = rng.integers(0, 9, n)
+    if kind == "skewed":
+        lens[::500] = 900                                   # padding blows past 2x -> CSR
+    m = _ragged_csr(n, lens, 12)
+    a = apps.SparseMatrix.from_csr(m, symmetric=False)
+    assert (a.sell_arrays() is None) == (kind == "skewed")
+    v = rng.standard_normal(n)
+    assert a.matvec(v).tobytes() == (m @ v).tobytes()
+    a._sell = False                                         # force the CSR kernel on the same matrix
+    assert a.matvec(v).tobytes() == (m @ v).tobytes()
+
+
 def test_vector_updates_match_numpy():
     rng = np.random.default_rng(5)
     a, b = rng.standard_normal(100001), rng.standard_normal(100001)
