@@ -250,8 +250,7 @@ def measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, norm, Q, config_
         _lib.check(lib.qdot_b200_begin(ws, s), lib)
         _lib.check(lib.qdot_b200_pass1(xc.data_ptr(), yc.data_ptr(), m, 0, ctypes.byref(c3), m, ws, s), lib)
         _lib.check(lib.qdot_b200_score_finalize(ws, m, ctypes.byref(c3), s), lib)
-        _lib.check(lib.qdot_b200_pass2(xc.data_ptr(), yc.data_ptr(), m, 0, ws, s), lib)
-        _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+        _lib.check(lib.qdot_b200_pass2_finalize(xc.data_ptr(), yc.data_ptr(), m, 0, ws, s), lib)
     for _ in range(3):
         c3_step()
     e0.record(stream)
@@ -357,12 +356,15 @@ def main():
             ev_p1[i][1].record(stream)
         if world > 1:
             reduce_regions(ra)                       # NCCL SUM of region A (histogram)
-        # one GPU: score also finalizes (no pass 2 here); N > 1: finalize after allreduce(B)
+        # one GPU: score finalizes when no pass 2 is needed, else the last pass-2
+        # CTA does (two launches); N > 1: finalize after the allreduce of region B
         _lib.check(score_fn(ws, n_total, ctypes.byref(c), s), lib)
-        _lib.check(lib.qdot_b200_pass2(xp, yp, n, norm, ws, s), lib)
-        if world > 1:
+        if world == 1:
+            _lib.check(lib.qdot_b200_pass2_finalize(xp, yp, n, norm, ws, s), lib)
+        else:
+            _lib.check(lib.qdot_b200_pass2(xp, yp, n, norm, ws, s), lib)
             reduce_regions(rb)                       # NCCL SUM of region B (exact partials)
-        _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+            _lib.check(lib.qdot_b200_finalize(ws, s), lib)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -471,7 +473,7 @@ def main():
             "value_check": value_check,
             "pass1_modes": pass1_modes,
             "clocks": clocks,
-            "gpu_launches": 4 * args.steps,
+            "gpu_launches": (3 if world == 1 else 4) * args.steps,   # pass1, score, pass2 (+ finalize at N > 1)
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -152,6 +152,10 @@ int qdot_b200_score_finalize(void* ws, int64_t n_total, const qdot_config* cfg, 
  * products for bins whose upper bound differs from the element's exponent
  * sum (ranged / split / early-terminated bins; emulate.py:137-153). */
 int qdot_b200_pass2(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream);
+/* single-device form of pass 2 + finalize in one launch: pass 2 when score
+ * flagged it, then the last CTA to finish finalizes (unless
+ * qdot_b200_score_finalize already did).  Not for multi-rank runs. */
+int qdot_b200_pass2_finalize(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream);
 /* per-bin values + ascending-upper Neumaier fold (emulate.py:154-163) */
 int qdot_b200_finalize(void* ws, void* stream);
 /* copy the result (and up to max_bins bins) to host memory; synchronises */

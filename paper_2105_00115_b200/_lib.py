@@ -74,6 +74,7 @@ SIGNATURES = {
     "qdot_b200_score": (_I, [_P, _I64, ctypes.POINTER(QdotConfig), _P]),
     "qdot_b200_score_finalize": (_I, [_P, _I64, ctypes.POINTER(QdotConfig), _P]),
     "qdot_b200_pass2": (_I, [_P, _P, _I64, _I, _P, _P]),
+    "qdot_b200_pass2_finalize": (_I, [_P, _P, _I64, _I, _P, _P]),
     "qdot_b200_finalize": (_I, [_P, _P]),
     "qdot_b200_fetch": (_I, [_P, ctypes.POINTER(QdotResult), ctypes.POINTER(QdotBin), ctypes.c_int32, _P]),
     "qdot_b200_dot": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _P, ctypes.POINTER(QdotResult),

@@ -338,8 +338,7 @@ class _IterGraph:
         _lib.check(lib.qdot_b200_begin(ws, stream), lib)
         _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(norm), ctypes.byref(c), n, ws, stream), lib)
         _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), stream), lib)
-        _lib.check(lib.qdot_b200_pass2(xp, yp, n, int(norm), ws, stream), lib)
-        _lib.check(lib.qdot_b200_finalize(ws, stream), lib)
+        _lib.check(lib.qdot_b200_pass2_finalize(xp, yp, n, int(norm), ws, stream), lib)
 
     def update(self, op: int, a, si: int, b, out, stream: int) -> None:
         """out = a + st[si]*b | a - st[si]*b | a / st[si]."""

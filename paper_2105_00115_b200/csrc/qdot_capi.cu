@@ -164,13 +164,23 @@ int qdot_b200_score_finalize(void* ws, int64_t n_total, const qdot_config* cfg, 
     return score_impl(ws, n_total, cfg, true, stream);
 }
 
-int qdot_b200_pass2(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream) {
+static int pass2_impl(const double* x, const double* y, int64_t n, int norm, void* ws, bool fin, void* stream) {
     if (!ws || n < 0 || (n > 0 && (!x || (!norm && !y)))) return QDOT_ERR_ARG;
     WsPtrs w = ws_ptrs(ws);
-    QD_CHECK(launch_pass2(x, norm ? x : y, n, norm != 0, w.lut_p2, w.meta, w.b, w.list, w.list_fill,
+    P2Fin f;
+    if (fin) { f.A = w.a; f.res = w.result; f.bins = w.bins; }
+    QD_CHECK(launch_pass2(x, norm ? x : y, n, norm != 0, w.lut_p2, w.meta, w.b, w.list, w.list_fill, f,
                           static_cast<cudaStream_t>(stream)),
              "pass2");
     return QDOT_OK;
+}
+
+int qdot_b200_pass2(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream) {
+    return pass2_impl(x, y, n, norm, ws, false, stream);
+}
+
+int qdot_b200_pass2_finalize(const double* x, const double* y, int64_t n, int norm, void* ws, void* stream) {
+    return pass2_impl(x, y, n, norm, ws, true, stream);
 }
 
 int qdot_b200_finalize(void* ws, void* stream) {
@@ -269,8 +279,7 @@ int enqueue_dot(const double* x, const double* y, int64_t n, int norm, const qdo
     if ((r = qdot_b200_begin(ws, s))) return r;
     if ((r = qdot_b200_pass1(x, y, n, norm, cfg, n, ws, s))) return r;
     if ((r = qdot_b200_score_finalize(ws, n, cfg, s))) return r;
-    if ((r = qdot_b200_pass2(x, y, n, norm, ws, s))) return r;
-    if ((r = qdot_b200_finalize(ws, s))) return r;
+    if ((r = qdot_b200_pass2_finalize(x, y, n, norm, ws, s))) return r;
     FastState& F = g_fast;
     QD_CHECK(launch_publish(static_cast<const char*>(ws) + OFF_RESULT, PUBLISH_BYTES, F.host_dev, F.dev_seq,
                             reinterpret_cast<uint32_t*>(F.host_dev + PUBLISH_BYTES), st), "publish");
@@ -437,8 +446,7 @@ int qdot_b200_dot_host(const double* hx, const double* hy, int64_t n, int norm, 
         if ((rc = qdot_b200_pass1(dx + off, norm ? nullptr : dy + off, len, norm, cfg, n, ws, ks))) break;
     }
     if (!rc) rc = qdot_b200_score_finalize(ws, n, cfg, ks);
-    if (!rc) rc = qdot_b200_pass2(dx, norm ? nullptr : dy, n, norm, ws, ks);
-    if (!rc) rc = qdot_b200_finalize(ws, ks);
+    if (!rc) rc = qdot_b200_pass2_finalize(dx, norm ? nullptr : dy, n, norm, ws, ks);
     if (!rc) rc = qdot_b200_fetch(ws, out, bins, max_bins, ks);
     cudaStreamSynchronize(ks);
     cudaStreamSynchronize(cs);

@@ -213,6 +213,24 @@ QD_HD int64_t double_units(uint64_t pb, int e) {
 }
 
 // ---- exact rounding -----------------------------------------------------------
+// m * 2^qq for a nonzero m < 2^54 whose value is exactly representable with
+// exponent <= 1023 (qq >= -1074): built from bits, no libm
+QD_HD double exact_scale(uint64_t m, int qq) {
+    const int tm = 63 - clz64(m);
+    const int E = tm + qq;                          // exponent of the leading bit
+    if (E >= -1022) {
+        const uint64_t frac = tm <= 52 ? (m << (52 - tm)) : (m >> (tm - 52));
+        return bitsd(((uint64_t)(E + 1023) << 52) | (frac & ((1ull << 52) - 1)));
+    }
+    return bitsd(m << (qq + 1074));                 // subnormal: exact since qq >= -1074
+}
+
+// 2^k as a double (0 below 2^-1074, inf above 2^1023), exact
+QD_HD double pow2d(int k) {
+    if (k >= -1022) return k > 1023 ? bitsd(0x7FF0000000000000ull) : bitsd((uint64_t)(k + 1023) << 52);
+    return k >= -1074 ? bitsd(1ull << (k + 1074)) : 0.0;
+}
+
 // Round (top + frac) * 2^q, frac in [0,1) nonzero iff `sticky`, to the binary
 // format with `mu` fraction bits and minimum normal exponent `emin`, maximum
 // exponent `emax`: round-to-nearest-even, gradual underflow, overflow -> inf.
@@ -241,7 +259,7 @@ QD_HD double round_scaled(uint64_t top, int q, bool sticky, bool neg, int mu, in
     if (m == 0) return neg ? -0.0 : 0.0;
     int tm = 63 - clz64(m);
     if (tm + qq > emax) { if (overflow) *overflow = 1; return neg ? -INFINITY : INFINITY; }
-    double r = ldexp((double)m, qq);             // exact: m <= 2^(mu+1), qq >= -1074
+    double r = exact_scale(m, qq);               // exact: m <= 2^(mu+1), qq >= -1074
     return neg ? -r : r;
 }
 

@@ -28,13 +28,29 @@ namespace qd {
 
 #include "qdot_pass1.cuh"
 
+// phase clocks of the score/finalize CTA (scripts/score_prof.cu builds with it)
+#ifdef QDOT_SCORE_PROFILE
+__device__ long long g_sc_prof[16];
+#define SC_STAMP(i) do { if (threadIdx.x == 0) g_sc_prof[i] = clock64(); } while (0)
+#else
+#define SC_STAMP(i) do { } while (0)
+#endif
+
 // =============================================================================
 // score (one CTA)
 // =============================================================================
 constexpr int SC_T = 1024;
 constexpr int SC_PER = (KEYS + SC_T - 1) / SC_T;   // 5 keys per thread
 
+// key rows staged in shared memory by the score CTA (cp.async, issued as soon
+// as [kmin, kmax] is known, consumed by the per-bin values and the LUT pass)
+constexpr int KR_D0 = 0, KR_S0 = 4, KR_H0 = 5, KR_INFP = 6, KR_INFN = 7, KR_HOT = 8, KR_PRIV = 9, KR_ROWS = 10;
+constexpr int KC_SPAN = 1024;   // keys cached: spans wider than this read global memory
+
 struct ScShared {
+    long long kc[KR_ROWS][KC_SPAN];     // key rows of [kmin, kmin + KC_SPAN)
+    double sval[KC_SPAN];               // per-bin values for the fold (cached path)
+    unsigned char sflag[KC_SPAN];       // per-bin flags (cached path)
     unsigned long long off[KEYS + 1];   // exclusive prefix of counts over keys
     long long bup[KEYS];                // per-bin upper bound (staged for the LUT pass)
     signed char bprec[KEYS];            // per-bin precision
@@ -43,7 +59,8 @@ struct ScShared {
     int bin_of[KEYS];
     unsigned long long red[SC_T / 32];
     long long red2[SC_T / 32];
-    int s_status, s_deg, s_early, s_nb, s_need;
+    int s_status, s_deg, s_early, s_nb, s_need, s_ovf, s_half;
+    unsigned long long s_cnt[4];
     int kmin, kmax;
     long long nnz;
     long long a_zero, a_listovf;
@@ -130,10 +147,240 @@ __device__ __forceinline__ long long floor_log2_d(double v, bool* ok) {    // sc
     return flexp_bits(dbits(v));
 }
 
+// =============================================================================
+// finalize (one CTA)
+// =============================================================================
+constexpr int FN_T = 256;
+
+__device__ __forceinline__ __int128 key_double(const int64_t* __restrict__ B, int k) {
+    __int128 v = (__int128)(unsigned long long)B[B_D0 + k];
+    v += (__int128)(unsigned long long)B[B_D1 + k] << 32;
+    v += (__int128)(unsigned long long)B[B_D2 + k] << 64;
+    v += (__int128)(long long)B[B_D3 + k] << 96;
+    return v;
+}
+
+// round an exact signed integer v * 2^lsb to a binary format (see round_scaled)
+__device__ __forceinline__ double round_i128(__int128 v, int lsb, int mu, int emin, int emax, int* ovf) {
+    if (v == 0) return 0.0;
+    const bool neg = v < 0;
+    unsigned __int128 a = neg ? (unsigned __int128)(-v) : (unsigned __int128)v;
+    const uint64_t hi = (uint64_t)(a >> 64);
+    if (!hi) return round_scaled((uint64_t)a, lsb, false, neg, mu, emin, emax, ovf);
+    const int sh = 64 - clz64(hi);                 // bits above the low 64
+    const uint64_t top = (uint64_t)(a >> sh);
+    const bool sticky = (a & (((unsigned __int128)1 << sh) - 1)) != 0;
+    return round_scaled(top, lsb + sh, sticky, neg, mu, emin, emax, ovf);
+}
+
+constexpr int FN_CHUNK = 1024;
+
+// key rows of the bin values: global memory (k_finalize, after pass 2) ...
+struct GlobalKeys {
+    const int64_t* __restrict__ A;
+    const int64_t* __restrict__ B;
+    const uint32_t* __restrict__ lut_p2;
+    __device__ __forceinline__ long long d(int i, int k) const { return B[B_D0 + i * (int64_t)KEYS + k]; }
+    __device__ __forceinline__ long long infp(int k) const { return B[B_INFP + k]; }
+    __device__ __forceinline__ long long infn(int k) const { return B[B_INFN + k]; }
+    __device__ __forceinline__ long long cnt(int k) const { return A[A_CNT + k]; }
+    __device__ __forceinline__ long long keyval(int k, bool half) const {
+        return (lut_p2[k] & P2_NEED) ? B[B_P2 + k] : (half ? B[B_H0 + k] : B[B_S0 + k]);
+    }
+};
+// ... or the score CTA's shared-memory cache (no pass 2: HALF/SINGLE sums are pass 1's)
+struct CachedKeys {
+    const long long* kc;                 // [KR_ROWS][KC_SPAN]
+    int k0;
+    const unsigned long long* off;       // exclusive prefix of counts
+    __device__ __forceinline__ long long d(int i, int k) const { return kc[(KR_D0 + i) * KC_SPAN + k - k0]; }
+    __device__ __forceinline__ long long infp(int k) const { return kc[KR_INFP * KC_SPAN + k - k0]; }
+    __device__ __forceinline__ long long infn(int k) const { return kc[KR_INFN * KC_SPAN + k - k0]; }
+    __device__ __forceinline__ long long cnt(int k) const { return (long long)(off[k + 1] - off[k]); }
+    __device__ __forceinline__ long long keyval(int k, bool half) const {
+        return kc[(half ? KR_H0 : KR_S0) * KC_SPAN + k - k0];
+    }
+};
+
+template <class K>
+__device__ __forceinline__ __int128 key_double(const K& kk, int k) {
+    __int128 v = (__int128)(unsigned long long)kk.d(0, k);
+    v += (__int128)(unsigned long long)kk.d(1, k) << 32;
+    v += (__int128)(unsigned long long)kk.d(2, k) << 64;
+    v += (__int128)(long long)kk.d(3, k) << 96;
+    return v;
+}
+
+// the value of one bin from its exact per-key sums, rounded like the
+// reference (emulate.py:116-154); *ovf: a HALF/SINGLE result overflowed,
+// *hf: a HALF bin whose fp32 sequential sum could depend on order
+template <class K>
+__device__ double bin_value(const K& kk, const qdot_bin& bn, int* ovf, int* hf) {
+    const int f = bn.first_key, l = bn.last_key;
+    const long long u = bn.upper;
+    double val = 0.0;
+    if (bn.precision == QDOT_DOUBLE) {                                      // emulate.py:132-133
+        long long ip = 0, in = 0;
+        for (int k = f; k <= l; ++k) { ip += kk.infp(k); in += kk.infn(k); }
+        int o = 0;
+        if (ip && in) val = __longlong_as_double(0x7FF8000000000000ll);
+        else if (ip) val = INFINITY;
+        else if (in) val = -INFINITY;
+        else if (f == l) val = round_i128(key_double(kk, f), qd_double(f - KOFF), 52, -1022, 1023, &o);
+        else {
+            BigSum<104> acc;
+            int lsb = qd_double(f - KOFF);
+            acc.init(lsb, (qd_double(l - KOFF) - lsb + 160) / 32 + 2);
+            for (int k = f; k <= l; ++k)
+                if (kk.cnt(k)) acc.add(key_double(kk, k), qd_double(k - KOFF));
+            val = acc.round(52, -1022, 1023, &o);
+        }
+    } else if (bn.precision != QDOT_PERFORATE) {                             // emulate.py:135-154
+        const bool half = bn.precision == QDOT_HALF;
+        const int mu = half ? 10 : 23;
+        const int qmin_fmt = half ? -24 : -149;
+        auto qs_of = [&](int k) {
+            long long d = u - (long long)(k - KOFF);
+            int dd = d > P2_DELTA_MAX ? P2_DELTA_MAX : (int)d;
+            return -dd - mu > qmin_fmt ? -dd - mu : qmin_fmt;
+        };
+        const int lsb = qs_of(f);
+        double mass = 0.0;   // bound on sum |p| (scaled domain) for the fp32-exactness check
+        double a;
+        int o = 0;
+        if (f == l) {
+            a = half ? round_i128((__int128)kk.keyval(f, half), lsb, 23, -126, 127, &o)
+                     : round_i128((__int128)kk.keyval(f, half), lsb, 52, -1022, 1023, &o);
+            long long d = u - (long long)(f - KOFF);
+            mass = (double)kk.cnt(f) * pow2d(2 - (int)(d > 2000 ? 2000 : d));
+        } else {
+            BigSum<16> acc;
+            acc.init(lsb, (qs_of(l) - lsb + 128) / 32 + 2);
+            for (int k = f; k <= l; ++k) {
+                long long c = kk.cnt(k);
+                if (!c) continue;
+                long long d = u - (long long)(k - KOFF);
+                acc.add((__int128)kk.keyval(k, half), qs_of(k));
+                mass += (double)c * pow2d(2 - (int)(d > 2000 ? 2000 : d));
+            }
+            a = half ? acc.round(23, -126, 127, &o) : acc.round(52, -1022, 1023, &o);
+        }
+        val = ldexp_rn(a, u, &o);                                             // emulate.py:154
+        if (o) *ovf = 1;
+        if (half && mass > pow2d(24 + lsb)) *hf = 1;
+    }
+    return val;
+}
+
+// qdot_accumulate: Neumaier over bins in ascending-upper order (emulate.py:55-72)
+__device__ __forceinline__ void neumaier_fold(const double* v, int cn, double& sum, double& c) {
+#pragma unroll 4
+    for (int i = 0; i < cn; ++i) {
+        const double x = v[i];
+        const double t = __dadd_rn(sum, x);
+        if (fabs(sum) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(sum, t), x));
+        else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), sum));
+        sum = t;
+    }
+}
+
+// per-thread precision counts -> shared totals (any block size)
+__device__ __forceinline__ void block_count_reduce(const long long (&cnt_local)[4], unsigned long long* s_cnt) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        long long v = cnt_local[p];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_cnt[p], (unsigned long long)v);
+    }
+}
+
+// the result header (kernel.py:175, scoring.py:192-216) and the phase times
+__device__ void write_result(unsigned long long ts0, unsigned long long ts1, const ScoreMeta& m, double sum, double c,
+                             const unsigned long long* s_cnt, int s_ovf, int s_half, qdot_result* __restrict__ res) {
+    qdot_result r;
+    memset(&r, 0, sizeof(r));
+    r.value = (sum - sum == 0.0) ? __dadd_rn(sum, c) : sum;
+    for (int i = 0; i < 4; ++i) r.counts[i] = (long long)s_cnt[i];
+    r.counts[QDOT_PERFORATE] += m.zero;                                        // kernel.py:175
+    r.eps_eff = m.eps_eff;
+    r.n = m.n_total;
+    r.nnz = m.nnz;
+    r.zero_count = m.zero;
+    r.status = m.status != QDOT_OK ? m.status : (s_ovf ? QDOT_ERR_OVERFLOW : QDOT_OK);
+    r.n_bins = m.n_bins;
+    r.e_min = m.e_min;
+    r.e_max = m.e_max;
+    r.early_terminated = m.early;
+    r.pass2_needed = m.need_p2;
+    r.half_order_sensitive = s_half;
+    const unsigned long long now = global_ns();
+    const unsigned long long sel = ts1 > ts0 ? ts1 - ts0 : 0ull, cmp = now > ts1 ? now - ts1 : 0ull;
+    r.select_ns = (int32_t)(sel < 0x7FFFFFFFull ? sel : 0x7FFFFFFFull);
+    r.compute_ns = (int32_t)(cmp < 0x7FFFFFFFull ? cmp : 0x7FFFFFFFull);
+    *res = r;
+}
+
+// per-bin values + Neumaier fold + result header from global memory; any
+// block size (k_finalize, and k_score when its key cache does not apply)
 __device__ void finalize_body(const int64_t* __restrict__ A, const int64_t* __restrict__ B,
                               const uint32_t* __restrict__ lut_p2, const ScoreMeta& m, qdot_result* __restrict__ res,
-                              qdot_bin* __restrict__ bins);
+                              qdot_bin* __restrict__ bins) {
+    const int nthr = blockDim.x;
+    __shared__ double s_val[FN_CHUNK];
+    __shared__ int s_ovf, s_half;
+    __shared__ double s_s, s_c;
+    __shared__ unsigned long long s_cnt[4];
+    const int tid = threadIdx.x;
+    if (tid == 0) { s_ovf = 0; s_half = 0; s_s = 0.0; s_c = 0.0; s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0; }
+    SC_STAMP(8);
+    __syncthreads();
+    const int nb = m.status == QDOT_OK ? m.n_bins : 0;
+    const GlobalKeys kk{A, B, lut_p2};
+    long long cnt_local[4] = {0, 0, 0, 0};   // per-thread precision counts (summed after the bins)
+    for (int base = 0; base < nb; base += FN_CHUNK) {
+        const int cn = nb - base < FN_CHUNK ? nb - base : FN_CHUNK;
+        for (int i = tid; i < cn; i += nthr) {
+            const int b = base + i;
+            const qdot_bin bn = bins[b];
+            int ovf = 0, hf = 0;
+            const double val = bin_value(kk, bn, &ovf, &hf);
+            if (ovf) atomicOr(&s_ovf, 1);
+            if (hf) atomicOr(&s_half, 1);
+            bins[b].value = val;
+            bins[b].flags = hf;
+            s_val[i] = val;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) cnt_local[p] += bn.precision == p ? bn.cardinality : 0;
+        }
+        __syncthreads();
+        SC_STAMP(9);
+        if (tid == 0) {
+            double sum = s_s, c = s_c;
+            neumaier_fold(s_val, cn, sum, c);
+            s_s = sum;
+            s_c = c;
+        }
+        __syncthreads();
+        SC_STAMP(10);
+    }
+    block_count_reduce(cnt_local, s_cnt);
+    __syncthreads();
+    SC_STAMP(11);
+    if (tid == 0) write_result(ws_stamps(A)[0], ws_stamps(A)[1], m, s_s, s_c, s_cnt, s_ovf, s_half, res);
+    SC_STAMP(12);
+}
 
+__global__ void __launch_bounds__(FN_T, 1)
+k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const uint32_t* __restrict__ lut_p2,
+           const ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
+    const ScoreMeta m = *meta;
+    if (m.done) return;
+    finalize_body(A, B, lut_p2, m, res, bins);
+}
+
+// =============================================================================
+// score (one CTA)
+// =============================================================================
 __global__ void __launch_bounds__(SC_T, 1)
 k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* __restrict__ lut_bin, uint32_t* __restrict__ lut_p2,
         ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins,
@@ -141,10 +388,15 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScShared& S = *reinterpret_cast<ScShared*>(smem_raw);
     const int tid = threadIdx.x;
+    SC_STAMP(0);
 
     // the flag words are loaded up front so their latency overlaps the counts'
     long long a_nonfinite = 0, a_zero = 0, a_listovf = 0;
-    if (tid == 0) { a_nonfinite = A[A_NONFINITE]; a_zero = A[A_ZERO]; a_listovf = A[A_LISTOVF]; }
+    unsigned long long ts0 = 0, ts1 = 0;
+    if (tid == 0) {
+        a_nonfinite = A[A_NONFINITE]; a_zero = A[A_ZERO]; a_listovf = A[A_LISTOVF];
+        ts0 = ws_stamps(A)[0];
+    }
     unsigned long long cnt[SC_PER];
     int kmin = KEYS, kmax = -1;
     unsigned long long tot = 0;
@@ -164,6 +416,20 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         kmin = (int)(r >> 16);
         kmax = KEYS - (int)(r & 0xFFFFu);
     }
+    // cached path: stage the key rows the bin values and the LUT read
+    const bool kcache = fuse && kmax >= kmin && kmax - kmin < KC_SPAN;
+    for (int j = tid; kcache && j <= kmax - kmin; j += SC_T) {
+        const int k = kmin + j;
+        const int64_t* src[KR_ROWS] = {B + B_D0 + k, B + B_D1 + k, B + B_D2 + k, B + B_D3 + k, B + B_S0 + k,
+                                       B + B_H0 + k, B + B_INFP + k, B + B_INFN + k, A + A_HOT + k, A + A_PRIV + k};
+#pragma unroll
+        for (int r = 0; r < KR_ROWS; ++r) {
+            const unsigned d = (unsigned)__cvta_generic_to_shared(&S.kc[r][j]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(src[r]) : "memory");
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    SC_STAMP(1);
     // exclusive prefix of counts -> off[]
     unsigned long long ex[SC_PER];
 #pragma unroll
@@ -192,8 +458,11 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         S.s_status = status; S.s_deg = deg; S.s_early = early;
         S.kmin = kmin; S.kmax = kmax; S.nnz = (long long)nnz;
         S.a_zero = a_zero; S.a_listovf = a_listovf;
+        S.s_ovf = 0; S.s_half = 0;
+        S.s_cnt[0] = S.s_cnt[1] = S.s_cnt[2] = S.s_cnt[3] = 0;
     }
     __syncthreads();
+    SC_STAMP(2);
     const int deg = S.s_deg, early = S.s_early;
     const int strategy = cfg.strategy;
 
@@ -276,6 +545,7 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         if (tid == 0) S.s_nb = 0;
     }
     __syncthreads();
+    SC_STAMP(3);
     const int nb = S.s_nb;
     if (tid == 0) {   // scoring.py:192-193
         double eps_eff = (cfg.split == 1 && nb) ? __ddiv_rn(cfg.epsilon, (double)nb) : cfg.epsilon;
@@ -285,10 +555,14 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         S.eps_eff = eps_eff;
         S.fl = fl;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    SC_STAMP(4);
     const int e_min = deg ? 0 : S.kmin - KOFF, e_max = deg ? 0 : S.kmax - KOFF;
 
     // ---- per-bin interval, score, precision (scoring.py:96-123, 181-199)
+    int my_ovf = 0, my_half = 0;
+    long long cnt_local[4] = {0, 0, 0, 0};
     for (int b = tid; b < nb; b += SC_T) {
         int f = S.first[b], l = S.last[b];
         long long M = (long long)(S.off[l + 1] - S.off[f]);
@@ -314,8 +588,20 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         bins[b] = ob;
         S.bup[b] = upper;
         S.bprec[b] = (signed char)ob.precision;
+        if (kcache) {   // speculative: valid when no pass 2 follows (then finalized below)
+            int ovf = 0, hf = 0;
+            SC_STAMP(9);
+            S.sval[b] = bin_value(CachedKeys{&S.kc[0][0], S.kmin, S.off}, ob, &ovf, &hf);
+            SC_STAMP(10);
+            S.sflag[b] = (unsigned char)hf;
+            my_ovf |= ovf;
+            my_half |= hf;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) cnt_local[p] += ob.precision == p ? M : 0;
+        }
     }
     __syncthreads();
+    SC_STAMP(5);
     __threadfence_block();
     // ---- LUTs.  need: some key needs pass 2; priv: such a key also has
     // elements accumulated in private windows (not in the cold-element list)
@@ -330,18 +616,23 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         if (b >= 0) {
             int pr = S.bprec[b];
             long long delta = S.bup[b] - (long long)(k - KOFF);
-            if ((pr == QDOT_HALF || pr == QDOT_SINGLE) && (delta > 0 || A[A_HOT + k] > 0) &&
-                S.s_status == QDOT_OK) {
+            const long long hot = kcache ? S.kc[KR_HOT][k - lut_lo] : A[A_HOT + k];
+            if ((pr == QDOT_HALF || pr == QDOT_SINGLE) && (delta > 0 || hot > 0) && S.s_status == QDOT_OK) {
                 d = P2_NEED | (pr == QDOT_HALF ? P2_HALF : 0u) |
                     (uint32_t)(delta > P2_DELTA_MAX ? P2_DELTA_MAX : delta);
                 need = 1;
-                if (A[A_PRIV + k] > 0) priv = 1;
+                if ((kcache ? S.kc[KR_PRIV][k - lut_lo] : A[A_PRIV + k]) > 0) priv = 1;
             }
         }
         lut_p2[k] = d;
     }
-    need = block_reduce<int>(need, reinterpret_cast<int*>(S.red2), [](int a, int b) { return a | b; }, 0);
-    priv = block_reduce<int>(priv, reinterpret_cast<int*>(S.red2), [](int a, int b) { return a | b; }, 0);
+    SC_STAMP(6);
+    {
+        const int np = block_reduce<int>(need | (priv << 1), reinterpret_cast<int*>(S.red2),
+                                         [](int a, int b) { return a | b; }, 0);
+        need = np & 1;
+        priv = np >> 1;
+    }
     // pass 2 mode: 2 = only over the cold-element list (every element of every
     // pass-2 key is in it, no slot overflowed), 1 = stream x and y again
     if (need) need = (!priv && S.a_listovf == 0) ? 2 : 1;
@@ -355,12 +646,32 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         sm = m;
         *meta = m;
     }
-    if (tid == 0) ws_stamps(A)[1] = global_ns();             // parameter selection done
+    if (tid == 0) { ts1 = global_ns(); ws_stamps(A)[1] = ts1; }   // parameter selection done
     __syncthreads();
+    SC_STAMP(7);
     // no pass 2 needed (the common case): finalize here and save a launch;
     // k_finalize then exits on meta->done
-    if (sm.done) finalize_body(A, B, lut_p2, sm, res, bins);
+    if (!sm.done) return;
+    if (!kcache) { finalize_body(A, B, lut_p2, sm, res, bins); return; }
+    // cached path: the bin values are already computed; fold + header
+    SC_STAMP(8);
+    const int nbv = sm.status == QDOT_OK ? nb : 0;
+    if (nbv) {
+        for (int b = tid; b < nbv; b += SC_T) { bins[b].value = S.sval[b]; bins[b].flags = S.sflag[b]; }
+        if (my_ovf) atomicOr(&S.s_ovf, 1);
+        if (my_half) atomicOr(&S.s_half, 1);
+        block_count_reduce(cnt_local, S.s_cnt);
+    }
+    __syncthreads();
+    SC_STAMP(11);
+    if (tid == 0) {
+        double sum = 0.0, c = 0.0;
+        neumaier_fold(S.sval, nbv, sum, c);
+        write_result(ts0, ts1, sm, sum, c, S.s_cnt, S.s_ovf, S.s_half, res);
+    }
+    SC_STAMP(12);
 }
+
 
 // =============================================================================
 // pass 2 (scaled HALF/SINGLE products for bins with upper > e)
@@ -413,14 +724,10 @@ __device__ __forceinline__ void p2_elem(P2Shared& S, double a, double b) {
 }
 
 template <bool NORM, bool VEC>
-__global__ void __launch_bounds__(P2_T)
-k_pass2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-        const uint32_t* __restrict__ lut_p2, const ScoreMeta* __restrict__ meta, int64_t* __restrict__ B,
-        const double2* __restrict__ list, const uint32_t* __restrict__ list_fill) {
-    const int mode = meta->need_p2;
-    if (!mode || meta->status != QDOT_OK) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    P2Shared& S = *reinterpret_cast<P2Shared*>(smem_raw);
+__device__ __forceinline__ void p2_body(P2Shared& S, const double* __restrict__ x, const double* __restrict__ y,
+                                        int64_t n, const uint32_t* __restrict__ lut_p2, int mode,
+                                        int64_t* __restrict__ B, const double2* __restrict__ list,
+                                        const uint32_t* __restrict__ list_fill) {
     const int tid = threadIdx.x;
     for (int k = tid; k < KEYS; k += P2_T) { S.acc[k] = 0ull; S.lut[k] = lut_p2[k]; }
     __syncthreads();
@@ -469,174 +776,35 @@ k_pass2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         if (S.acc[k]) atomicAdd(reinterpret_cast<unsigned long long*>(B + B_P2 + k), S.acc[k]);
 }
 
-// =============================================================================
-// finalize (one CTA)
-// =============================================================================
-constexpr int FN_T = 256;
-
-__device__ __forceinline__ __int128 key_double(const int64_t* __restrict__ B, int k) {
-    __int128 v = (__int128)(unsigned long long)B[B_D0 + k];
-    v += (__int128)(unsigned long long)B[B_D1 + k] << 32;
-    v += (__int128)(unsigned long long)B[B_D2 + k] << 64;
-    v += (__int128)(long long)B[B_D3 + k] << 96;
-    return v;
-}
-
-// round an exact signed integer v * 2^lsb to a binary format (see round_scaled)
-__device__ __forceinline__ double round_i128(__int128 v, int lsb, int mu, int emin, int emax, int* ovf) {
-    if (v == 0) return 0.0;
-    const bool neg = v < 0;
-    unsigned __int128 a = neg ? (unsigned __int128)(-v) : (unsigned __int128)v;
-    const uint64_t hi = (uint64_t)(a >> 64);
-    if (!hi) return round_scaled((uint64_t)a, lsb, false, neg, mu, emin, emax, ovf);
-    const int sh = 64 - clz64(hi);                 // bits above the low 64
-    const uint64_t top = (uint64_t)(a >> sh);
-    const bool sticky = (a & (((unsigned __int128)1 << sh) - 1)) != 0;
-    return round_scaled(top, lsb + sh, sticky, neg, mu, emin, emax, ovf);
-}
-
-constexpr int FN_CHUNK = 1024;
-
-// per-bin values + Neumaier fold + result header; any block size (called by
-// k_score with 1024 threads and by k_finalize with FN_T)
-__device__ void finalize_body(const int64_t* __restrict__ A, const int64_t* __restrict__ B,
-                              const uint32_t* __restrict__ lut_p2, const ScoreMeta& m, qdot_result* __restrict__ res,
-                              qdot_bin* __restrict__ bins) {
-    const int nthr = blockDim.x;
-    __shared__ double s_val[FN_CHUNK];
-    __shared__ int s_ovf, s_half;
-    __shared__ double s_s, s_c;
-    __shared__ long long s_cnt[4];
+template <bool NORM, bool VEC>
+__global__ void __launch_bounds__(P2_T)
+k_pass2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+        const uint32_t* __restrict__ lut_p2, const ScoreMeta* __restrict__ meta, int64_t* __restrict__ B,
+        const double2* __restrict__ list, const uint32_t* __restrict__ list_fill, int fin,
+        const int64_t* __restrict__ A, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
+    const int mode = meta->need_p2;
+    const bool work = mode && meta->status == QDOT_OK;
+    // fin: the last CTA to finish also finalizes (unless score already did)
+    const bool finish = fin && !meta->done;
+    if (!work && !finish) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    P2Shared& S = *reinterpret_cast<P2Shared*>(smem_raw);
     const int tid = threadIdx.x;
-    if (tid == 0) { s_ovf = 0; s_half = 0; s_s = 0.0; s_c = 0.0; s_cnt[0] = s_cnt[1] = s_cnt[2] = s_cnt[3] = 0; }
-    __syncthreads();
-    const int nb = m.status == QDOT_OK ? m.n_bins : 0;
-    long long cnt_local[4] = {0, 0, 0, 0};   // per-thread precision counts (summed after the bins)
-    for (int base = 0; base < nb; base += FN_CHUNK) {
-        const int cn = nb - base < FN_CHUNK ? nb - base : FN_CHUNK;
-        for (int i = tid; i < cn; i += nthr) {
-            const int b = base + i;
-            const qdot_bin bn = bins[b];
-            const int f = bn.first_key, l = bn.last_key;
-            const long long u = bn.upper;
-            double val = 0.0;
-            int flags = 0;
-            if (bn.precision == QDOT_DOUBLE) {                                  // emulate.py:132-133
-                long long ip = 0, in = 0;
-                for (int k = f; k <= l; ++k) { ip += B[B_INFP + k]; in += B[B_INFN + k]; }
-                int ovf = 0;
-                if (ip && in) val = __longlong_as_double(0x7FF8000000000000ll);
-                else if (ip) val = INFINITY;
-                else if (in) val = -INFINITY;
-                else if (f == l) val = round_i128(key_double(B, f), qd_double(f - KOFF), 52, -1022, 1023, &ovf);
-                else {
-                    BigSum<104> acc;
-                    int lsb = qd_double(f - KOFF);
-                    acc.init(lsb, (qd_double(l - KOFF) - lsb + 160) / 32 + 2);
-                    for (int k = f; k <= l; ++k)
-                        if (A[A_CNT + k]) acc.add(key_double(B, k), qd_double(k - KOFF));
-                    val = acc.round(52, -1022, 1023, &ovf);
-                }
-            } else if (bn.precision != QDOT_PERFORATE) {                         // emulate.py:135-154
-                const bool half = bn.precision == QDOT_HALF;
-                const int mu = half ? 10 : 23;
-                const int qmin_fmt = half ? -24 : -149;
-                auto qs_of = [&](int k) {
-                    long long d = u - (long long)(k - KOFF);
-                    int dd = d > P2_DELTA_MAX ? P2_DELTA_MAX : (int)d;
-                    return -dd - mu > qmin_fmt ? -dd - mu : qmin_fmt;
-                };
-                auto keyval = [&](int k) -> long long {
-                    return (lut_p2[k] & P2_NEED) ? B[B_P2 + k] : (half ? B[B_H0 + k] : B[B_S0 + k]);
-                };
-                const int lsb = qs_of(f);
-                double mass = 0.0;   // bound on sum |p| (scaled domain) for the fp32-exactness check
-                double a;
-                int ovf = 0;
-                if (f == l) {
-                    a = half ? round_i128((__int128)keyval(f), lsb, 23, -126, 127, &ovf)
-                             : round_i128((__int128)keyval(f), lsb, 52, -1022, 1023, &ovf);
-                    long long d = u - (long long)(f - KOFF);
-                    mass = (double)A[A_CNT + f] * ldexp(4.0, (int)(d > 2000 ? -2000 : -d));
-                } else {
-                    BigSum<16> acc;
-                    acc.init(lsb, (qs_of(l) - lsb + 128) / 32 + 2);
-                    for (int k = f; k <= l; ++k) {
-                        long long c = A[A_CNT + k];
-                        if (!c) continue;
-                        long long d = u - (long long)(k - KOFF);
-                        acc.add((__int128)keyval(k), qs_of(k));
-                        mass += (double)c * ldexp(4.0, (int)(d > 2000 ? -2000 : -d));
-                    }
-                    a = half ? acc.round(23, -126, 127, &ovf) : acc.round(52, -1022, 1023, &ovf);
-                }
-                val = ldexp_rn(a, u, &ovf);                                       // emulate.py:154
-                if (ovf) atomicOr(&s_ovf, 1);
-                if (half && mass > ldexp(1.0, 24 + lsb)) { flags |= 1; atomicOr(&s_half, 1); }
-            }
-            bins[b].value = val;
-            bins[b].flags = flags;
-            s_val[i] = val;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) cnt_local[p] += bn.precision == p ? bn.cardinality : 0;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            // qdot_accumulate: Neumaier over bins in ascending-upper order (emulate.py:55-72)
-            double sum = s_s, c = s_c;
-#pragma unroll 4
-            for (int i = 0; i < cn; ++i) {
-                const double v = s_val[i];
-                const double t = __dadd_rn(sum, v);
-                if (fabs(sum) >= fabs(v)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(sum, t), v));
-                else c = __dadd_rn(c, __dadd_rn(__dsub_rn(v, t), sum));
-                sum = t;
-            }
-            s_s = sum;
-            s_c = c;
-        }
-        __syncthreads();
-    }
-    for (int p = 0; p < 4; ++p) {
-        long long v = cnt_local[p];
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((tid & 31) == 0 && v) atomicAdd(reinterpret_cast<unsigned long long*>(&s_cnt[p]), (unsigned long long)v);
-    }
+    if (work) p2_body<NORM, VEC>(S, x, y, n, lut_p2, mode, B, list, list_fill);
+    if (!finish) return;
+    __threadfence();
     __syncthreads();
     if (tid == 0) {
-        qdot_result r;
-        memset(&r, 0, sizeof(r));
-        const double sum = s_s;
-        r.value = (sum - sum == 0.0) ? __dadd_rn(sum, s_c) : sum;
-        for (int i = 0; i < 4; ++i) r.counts[i] = s_cnt[i];
-        r.counts[QDOT_PERFORATE] += m.zero;                                    // kernel.py:175
-        r.eps_eff = m.eps_eff;
-        r.n = m.n_total;
-        r.nnz = m.nnz;
-        r.zero_count = m.zero;
-        r.status = m.status != QDOT_OK ? m.status : (s_ovf ? QDOT_ERR_OVERFLOW : QDOT_OK);
-        r.n_bins = m.n_bins;
-        r.e_min = m.e_min;
-        r.e_max = m.e_max;
-        r.early_terminated = m.early;
-        r.pass2_needed = m.need_p2;
-        r.half_order_sensitive = s_half;
-        const unsigned long long* ts = ws_stamps(A);
-        const unsigned long long now = global_ns();
-        const unsigned long long sel = ts[1] > ts[0] ? ts[1] - ts[0] : 0ull, cmp = now > ts[1] ? now - ts[1] : 0ull;
-        r.select_ns = (int32_t)(sel < 0x7FFFFFFFull ? sel : 0x7FFFFFFFull);
-        r.compute_ns = (int32_t)(cmp < 0x7FFFFFFFull ? cmp : 0x7FFFFFFFull);
-        *res = r;
+        unsigned long long* ticket = ws_stamps(A) + 4;     // zeroed by begin
+        S.need = atomicAdd(ticket, 1ull) == gridDim.x - 1ull;
     }
-}
-
-__global__ void __launch_bounds__(FN_T, 1)
-k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const uint32_t* __restrict__ lut_p2,
-           const ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
+    __syncthreads();
+    if (!S.need) return;
+    __threadfence();
     const ScoreMeta m = *meta;
-    if (m.done) return;
     finalize_body(A, B, lut_p2, m, res, bins);
 }
+
 
 #include "qdot_batched.cuh"
 
@@ -752,10 +920,16 @@ cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, u
     return cudaGetLastError();
 }
 
+cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
+                            qdot_result* res, qdot_bin* bins, cudaStream_t st) {
+    k_finalize<<<1, FN_T, 0, st>>>(A, B, lut_p2, meta, res, bins);
+    return cudaGetLastError();
+}
+
 template <bool NORM, bool VEC>
 static cudaError_t launch_pass2_t(const double* x, const double* y, int64_t n, const uint32_t* lut_p2,
                                   const ScoreMeta* meta, int64_t* B, const double2* list, const uint32_t* list_fill,
-                                  cudaStream_t st) {
+                                  const P2Fin& fin, cudaStream_t st) {
     auto kern = k_pass2<NORM, VEC>;
     const size_t smem = sizeof(P2Shared);
     static bool attr = false;
@@ -769,26 +943,22 @@ static cudaError_t launch_pass2_t(const double* x, const double* y, int64_t n, c
     int64_t grid = (int64_t)sm_count_cached() * occ;
     if (grid > ntiles) grid = ntiles;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, P2_T, smem, st>>>(x, y, n, lut_p2, meta, B, list, list_fill);
+    kern<<<(unsigned)grid, P2_T, smem, st>>>(x, y, n, lut_p2, meta, B, list, list_fill, fin.A ? 1 : 0, fin.A,
+                                             fin.res, fin.bins);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm, const uint32_t* lut_p2,
                          const ScoreMeta* meta, int64_t* B, const double2* list, const uint32_t* list_fill,
-                         cudaStream_t st) {
-    if (n <= 0) return cudaSuccess;
+                         const P2Fin& fin, cudaStream_t st) {
+    if (n <= 0) return fin.A ? launch_finalize(fin.A, B, lut_p2, meta, fin.res, fin.bins, st) : cudaSuccess;
     bool vec = ((reinterpret_cast<uintptr_t>(x) | (norm ? 0 : reinterpret_cast<uintptr_t>(y))) & 15u) == 0;
-    if (norm) return vec ? launch_pass2_t<true, true>(x, x, n, lut_p2, meta, B, list, list_fill, st)
-                         : launch_pass2_t<true, false>(x, x, n, lut_p2, meta, B, list, list_fill, st);
-    return vec ? launch_pass2_t<false, true>(x, y, n, lut_p2, meta, B, list, list_fill, st)
-               : launch_pass2_t<false, false>(x, y, n, lut_p2, meta, B, list, list_fill, st);
+    if (norm) return vec ? launch_pass2_t<true, true>(x, x, n, lut_p2, meta, B, list, list_fill, fin, st)
+                         : launch_pass2_t<true, false>(x, x, n, lut_p2, meta, B, list, list_fill, fin, st);
+    return vec ? launch_pass2_t<false, true>(x, y, n, lut_p2, meta, B, list, list_fill, fin, st)
+               : launch_pass2_t<false, false>(x, y, n, lut_p2, meta, B, list, list_fill, fin, st);
 }
 
-cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
-                            qdot_result* res, qdot_bin* bins, cudaStream_t st) {
-    k_finalize<<<1, FN_T, 0, st>>>(A, B, lut_p2, meta, res, bins);
-    return cudaGetLastError();
-}
 
 // copy the result header and the first `nbins` bins into host-mapped memory,
 // then bump the sequence word the host spins on (written last, after a
@@ -864,3 +1034,9 @@ cudaError_t launch_bin_ids(const double* x, const double* y, int64_t n, bool nor
 }
 
 }  // namespace qd
+
+#ifdef QDOT_SCORE_PROFILE
+extern "C" int qdot_b200_score_prof(long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, qd::g_sc_prof, sizeof(long long) * 16);
+}
+#endif

@@ -16,9 +16,16 @@ cudaError_t launch_pass1(const double* x, const double* y, int64_t n, bool norm,
 cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta,
                          qdot_result* res, qdot_bin* bins, int64_t n_total, const qdot_config& cfg,
                          bool fuse_finalize, cudaStream_t st);
+// fin.A != nullptr: the last pass-2 CTA also finalizes (one GPU: no exchange
+// of region B between pass 2 and finalize)
+struct P2Fin {
+    const int64_t* A = nullptr;
+    qdot_result* res = nullptr;
+    qdot_bin* bins = nullptr;
+};
 cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm, const uint32_t* lut_p2,
                          const ScoreMeta* meta, int64_t* B, const double2* list, const uint32_t* list_fill,
-                         cudaStream_t st);
+                         const P2Fin& fin, cudaStream_t st);
 cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
                             qdot_result* res, qdot_bin* bins, cudaStream_t st);
 cudaError_t launch_publish(const void* block, int nbytes, void* host_dev, uint32_t* dev_seq, uint32_t* host_seq_dev,

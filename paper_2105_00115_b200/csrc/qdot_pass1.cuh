@@ -386,8 +386,15 @@ template <bool NORM>
 __device__ __forceinline__ void p1_prefetch_l2(const double* x, const double* y, int64_t n, int64_t tile, int TILE) {
     const int64_t e0 = tile * TILE;
     if (e0 + TILE > n) return;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(x + e0), "r"(TILE * 8) : "memory");
-    if (!NORM) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(y + e0), "r"(TILE * 8) : "memory");
+    // evict-first: the streamed lines go before the workspace tables and the
+    // code of the kernels that follow (score / finalize run cold otherwise)
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(x + e0), "r"(TILE * 8), "l"(pol)
+                 : "memory");
+    if (!NORM)
+        asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(y + e0), "r"(TILE * 8),
+                     "l"(pol) : "memory");
 }
 
 // persistent loop over tiles.  PF: register double buffering (the loads of

@@ -123,8 +123,7 @@ def run_device(xd, yd, n: int, norm: bool, cfg: ToleranceConfig, strategy, st=No
     _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), s), lib)
     if torch_stream is not None:
         st.ev[1].record(torch_stream)
-    _lib.check(lib.qdot_b200_pass2(xp, yp, n, int(norm), ws, s), lib)
-    _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+    _lib.check(lib.qdot_b200_pass2_finalize(xp, yp, n, int(norm), ws, s), lib)
     if torch_stream is not None:
         st.ev[2].record(torch_stream)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
@@ -213,8 +212,7 @@ def select_parameters(x, y, cfg: ToleranceConfig, strategy: Strategy = None) -> 
     _lib.check(lib.qdot_b200_pass1(xd.data_ptr(), yd.data_ptr(), n, int(is_norm), ctypes.byref(c), n, ws, s), lib)
     _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), s), lib)
     # finalize also fills the result header and per-bin values; cheap (1 CTA)
-    _lib.check(lib.qdot_b200_pass2(xd.data_ptr(), yd.data_ptr(), n, int(is_norm), ws, s), lib)
-    _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+    _lib.check(lib.qdot_b200_pass2_finalize(xd.data_ptr(), yd.data_ptr(), n, int(is_norm), ws, s), lib)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
     res = st.result
     _raise_status(res)
@@ -329,8 +327,7 @@ def _run_host_pipelined(xh, yh, norm: bool, cfg: ToleranceConfig, strategy):
     _lib.check(lib.qdot_b200_begin(ws, s), lib)
     xd, yd = h2d_pass1(xh, yh, norm, c, n, st, device)
     _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), s), lib)
-    _lib.check(lib.qdot_b200_pass2(xd.data_ptr(), yd.data_ptr(), n, int(norm), ws, s), lib)
-    _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+    _lib.check(lib.qdot_b200_pass2_finalize(xd.data_ptr(), yd.data_ptr(), n, int(norm), ws, s), lib)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
     res = st.result
     phase = {"select": int(res.select_ns), "compute": int(res.compute_ns), "reference": 0}

@@ -11,7 +11,7 @@ dev = torch.device("cuda", 0)
 x = torch.randn(n, dtype=torch.float64, device=dev); y = torch.randn(n, dtype=torch.float64, device=dev)
 lib = _lib.load(); st = thread_state(dev); c = config_struct(Q.ToleranceConfig(1e-8), Q.ExactBinning())
 s = torch.cuda.current_stream(); sp = s.cuda_stream; ws = st.ws_ptr; cr = ctypes.byref(c)
-names = ["begin", "pass1", "score+fin", "pass2", "finalize"]
+names = ["begin", "pass1", "score+fin", "pass2+fin", "(none)"]
 R = 200
 evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(R)]
 for it in range(R + 20):
@@ -23,9 +23,9 @@ for it in range(R + 20):
     if e: e[2].record(s)
     lib.qdot_b200_score_finalize(ws, n, cr, sp)
     if e: e[3].record(s)
-    lib.qdot_b200_pass2(x.data_ptr(), y.data_ptr(), n, 0, ws, sp)
+    lib.qdot_b200_pass2_finalize(x.data_ptr(), y.data_ptr(), n, 0, ws, sp)
     if e: e[4].record(s)
-    lib.qdot_b200_finalize(ws, sp)
+    pass
     if e: e[5].record(s)
 torch.cuda.synchronize()
 tot = [0.0] * 5

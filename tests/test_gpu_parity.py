@@ -376,3 +376,50 @@ def test_graph_one_call_path_small(n):
         assert res.status == 0 and res.n_bins == ref.n_bins
         assert res.value == ref.value or (n == 0 and res.value == 0.0)
         assert [bins[i].cardinality for i in range(res.n_bins)] == [b.cardinality for b in ref.bins]
+
+
+@pytest.mark.parametrize("strategy,eps", [("exact", 1e-8), ("ranged:3", 1e-8), ("split:4", 1e-6), ("ranged:8", 1e-4)])
+@pytest.mark.parametrize("n", [0, 1000, 300001])
+def test_pass2_finalize_sequences_agree(strategy, eps, n):
+    """The three single-device launch sequences give byte-identical results:
+    score + pass2 + finalize (staged), score_finalize + pass2_finalize (fused:
+    score or the last pass-2 CTA finalizes), score + pass2_finalize."""
+    import ctypes
+    from paper_2105_00115_b200 import _lib
+    from paper_2105_00115_b200.device import config_struct, thread_state
+    rng = np.random.default_rng(n + 17)
+    x = torch.from_numpy(rng.standard_normal(n) * np.exp2(rng.integers(-30, 30, n))).cuda()
+    y = torch.from_numpy(rng.standard_normal(n)).cuda()
+    lib = _lib.load()
+    st = thread_state(x.device)
+    ws = st.ws_ptr
+    s = torch.cuda.current_stream().cuda_stream
+    c = config_struct(Q.ToleranceConfig(eps), strat(strategy))
+    xp, yp = (x.data_ptr(), y.data_ptr()) if n else (0, 0)
+    outs = []
+    for seq in ("staged", "fused", "score+p2fin"):
+        _lib.check(lib.qdot_b200_begin(ws, s), lib)
+        _lib.check(lib.qdot_b200_pass1(xp, yp, n, 0, ctypes.byref(c), n, ws, s), lib)
+        if seq == "fused":
+            _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), s), lib)
+        else:
+            _lib.check(lib.qdot_b200_score(ws, n, ctypes.byref(c), s), lib)
+        if seq == "staged":
+            _lib.check(lib.qdot_b200_pass2(xp, yp, n, 0, ws, s), lib)
+            _lib.check(lib.qdot_b200_finalize(ws, s), lib)
+        else:
+            _lib.check(lib.qdot_b200_pass2_finalize(xp, yp, n, 0, ws, s), lib)
+        res = _lib.QdotResult()
+        bins = (_lib.QdotBin * (_lib.KEYS + 1))()
+        _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(res), bins, _lib.KEYS + 1, s), lib)
+        torch.cuda.synchronize()
+        nb = res.n_bins
+        outs.append((res.value, res.status, res.n_bins, tuple(res.counts), res.pass2_needed, res.half_order_sensitive,
+                     ctypes.string_at(ctypes.addressof(bins), nb * ctypes.sizeof(_lib.QdotBin))))
+    assert outs[0] == outs[1] == outs[2]
+    if n:
+        ref = O.qdot(x.cpu().numpy(), y.cpu().numpy(), eps, "none", 52, strategy)
+        if outs[0][5]:   # a HALF bin the reference sums order-sensitively in fp32: its budget applies
+            assert abs(outs[0][0] - ref.value) <= ref.abs_cap
+        else:
+            assert outs[0][0] == ref.value
