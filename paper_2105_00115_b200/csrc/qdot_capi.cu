@@ -113,7 +113,8 @@ int qdot_b200_begin(void* ws, void* stream) {
     if (!ws) return QDOT_ERR_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // regions A and B are contiguous
-    QD_CHECK(cudaMemsetAsync(static_cast<char*>(ws) + OFF_A, 0, (size_t)(BYTES_A + BYTES_B + BYTES_LOCAL), st), "memset");
+    static_assert((BYTES_A + BYTES_B + BYTES_LOCAL) % 16 == 0 && OFF_A % 16 == 0, "begin zeroes 16-byte words");
+    QD_CHECK(launch_begin(static_cast<char*>(ws) + OFF_A, (size_t)(BYTES_A + BYTES_B + BYTES_LOCAL), st), "begin");
     return QDOT_OK;
 }
 

@@ -110,6 +110,12 @@ __device__ __forceinline__ unsigned long long* ws_stamps(const int64_t* A) {
     return reinterpret_cast<unsigned long long*>(
         reinterpret_cast<char*>(const_cast<int64_t*>(A)) - OFF_A + OFF_LOCAL + LIST_SLOTS * 4);
 }
+// programmatic dependent launch (the kernels of one call are launched with
+// programmatic stream serialization): a kernel may start while its
+// predecessor drains, and waits here before touching the workspace
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

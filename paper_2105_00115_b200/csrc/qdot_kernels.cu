@@ -388,6 +388,8 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScShared& S = *reinterpret_cast<ScShared*>(smem_raw);
     const int tid = threadIdx.x;
+    pdl_wait();
+    pdl_trigger();
     SC_STAMP(0);
 
     // the flag words are loaded up front so their latency overlaps the counts'
@@ -782,6 +784,7 @@ k_pass2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         const uint32_t* __restrict__ lut_p2, const ScoreMeta* __restrict__ meta, int64_t* __restrict__ B,
         const double2* __restrict__ list, const uint32_t* __restrict__ list_fill, int fin,
         const int64_t* __restrict__ A, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins) {
+    pdl_wait();
     const int mode = meta->need_p2;
     const bool work = mode && meta->status == QDOT_OK;
     // fin: the last CTA to finish also finalizes (unless score already did)
@@ -825,6 +828,43 @@ __global__ void k_bin_ids(const double* __restrict__ x, const double* __restrict
 // =============================================================================
 // launchers
 // =============================================================================
+// launch with programmatic stream serialization (QDOT_B200_PDL=0 disables):
+// the kernel may begin while its predecessor in the stream drains and calls
+// pdl_wait() before it touches anything that predecessor writes
+static bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("QDOT_B200_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(block);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
+}
+
+// zero regions A, B and the rank-local counters (replaces a memset so that
+// pass 1, launched after it with programmatic serialization, can sample its
+// inputs while this runs); launched normally: it waits for all prior work
+__global__ void __launch_bounds__(256) k_begin(ulonglong2* __restrict__ p, int64_t n16) {
+    pdl_trigger();
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n16; i += (int64_t)gridDim.x * 256)
+        p[i] = make_ulonglong2(0ull, 0ull);
+}
+
 static int sm_count_cached() {
     static int sms = 0;
     if (!sms) {
@@ -860,8 +900,7 @@ static cudaError_t launch_pass1_t(const double* x, const double* y, int64_t n, i
     int64_t grid = (int64_t)sm_count_cached() * occ;
     if (grid > ntiles) grid = ntiles;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, P1_T, smem, st>>>(x, y, n, A, B, prm);
-    return cudaGetLastError();
+    return launch_pdl(kern, (unsigned)grid, P1_T, smem, st, x, y, n, A, B, prm);
 }
 
 #ifdef QDOT_B200_P1_TUNING
@@ -916,7 +955,14 @@ cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, u
         cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    k_score<<<1, SC_T, smem, st>>>(A, B, lut_bin, lut_p2, meta, res, bins, n_total, cfg, fuse ? 1 : 0);
+    return launch_pdl(k_score, 1, SC_T, smem, st, A, B, lut_bin, lut_p2, meta, res, bins, n_total, cfg, fuse ? 1 : 0);
+}
+
+cudaError_t launch_begin(void* region, size_t bytes, cudaStream_t st) {
+    const int64_t n16 = (int64_t)(bytes / 16);
+    int64_t grid = (n16 + 255) / 256;
+    if (grid > sm_count_cached()) grid = sm_count_cached();
+    k_begin<<<(unsigned)(grid < 1 ? 1 : grid), 256, 0, st>>>(static_cast<ulonglong2*>(region), n16);
     return cudaGetLastError();
 }
 
@@ -943,9 +989,8 @@ static cudaError_t launch_pass2_t(const double* x, const double* y, int64_t n, c
     int64_t grid = (int64_t)sm_count_cached() * occ;
     if (grid > ntiles) grid = ntiles;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, P2_T, smem, st>>>(x, y, n, lut_p2, meta, B, list, list_fill, fin.A ? 1 : 0, fin.A,
-                                             fin.res, fin.bins);
-    return cudaGetLastError();
+    return launch_pdl(kern, (unsigned)grid, P2_T, smem, st, x, y, n, lut_p2, meta, B, list, list_fill, fin.A ? 1 : 0,
+                      fin.A, fin.res, fin.bins);
 }
 
 cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm, const uint32_t* lut_p2,

@@ -26,6 +26,8 @@ struct P2Fin {
 cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm, const uint32_t* lut_p2,
                          const ScoreMeta* meta, int64_t* B, const double2* list, const uint32_t* list_fill,
                          const P2Fin& fin, cudaStream_t st);
+// zero `bytes` (a multiple of 16, 16-byte aligned) at region: regions A, B, local
+cudaError_t launch_begin(void* region, size_t bytes, cudaStream_t st);
 cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,
                             qdot_result* res, qdot_bin* bins, cudaStream_t st);
 cudaError_t launch_publish(const void* block, int nbytes, void* host_dev, uint32_t* dev_seq, uint32_t* host_seq_dev,

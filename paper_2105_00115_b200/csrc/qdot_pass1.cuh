@@ -462,7 +462,7 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     const int tid = threadIdx.x;
     constexpr int TILE = P1_T * 2 * V;
     const int64_t ntiles = (n + TILE - 1) / TILE;
-    if (blockIdx.x == 0 && tid == 0) atomicCAS(ws_stamps(A), 0ull, global_ns());   // first launch only
+    pdl_trigger();   // score may be scheduled as SMs drain; it waits for this grid
 
     if (SMALL) {
         // short inputs: the window only has to be reasonable -- [kmax - W + 3,
@@ -482,6 +482,8 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         }
         kmx = __reduce_max_sync(0xffffffffu, kmx);
         if ((tid & 31) == 0) S.red[tid >> 5] = (unsigned long long)(long long)kmx;
+        pdl_wait();      // the sampling above reads only x, y; the workspace comes next
+        if (blockIdx.x == 0 && tid == 0) atomicCAS(ws_stamps(A), 0ull, global_ns());   // first launch only
         __syncthreads();
         if (tid == 0) {
             int m = -1;
@@ -522,6 +524,8 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                 if (fx - 1u < 0x7FEu && fy - 1u < 0x7FEu) atomicAdd(&hist[(int)(fx + fy) - 2046 + KOFF], 1u);
             }
         }
+        pdl_wait();      // the sampling above reads only x, y; the workspace comes next
+        if (blockIdx.x == 0 && tid == 0) atomicCAS(ws_stamps(A), 0ull, global_ns());   // first launch only
         __syncthreads();
         {   // inclusive prefix over KEYS (17 keys per thread) + largest sampled key
             constexpr int PER = (KEYS + P1_T - 1) / P1_T;
