@@ -928,6 +928,10 @@ static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, i
         case 2: return launch_pass1_t<NORM, VEC, 2, false, 3>(x, y, n, A, B, prm, st);
         case 3: return launch_pass1_t<NORM, VEC, 4, false, 2>(x, y, n, A, B, prm, st);
         case 4: return launch_pass1_t<NORM, VEC, 2, true, 0>(x, y, n, A, B, prm, st);    // register double buffer
+        case 5: return launch_pass1_t<NORM, VEC, 4, false, 5>(x, y, n, A, B, prm, st);
+        case 6: return launch_pass1_t<NORM, VEC, 4, false, 7>(x, y, n, A, B, prm, st);
+        case 7: return launch_pass1_t<NORM, VEC, 2, false, 6>(x, y, n, A, B, prm, st);
+        case 8: return launch_pass1_t<NORM, VEC, 2, false, 10>(x, y, n, A, B, prm, st);
         default: break;
     }
 #endif

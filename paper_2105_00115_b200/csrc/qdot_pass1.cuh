@@ -389,7 +389,11 @@ __device__ __forceinline__ void p1_prefetch_l2(const double* x, const double* y,
     // evict-first: the streamed lines go before the workspace tables and the
     // code of the kernels that follow (score / finalize run cold otherwise)
     uint64_t pol;
+#ifdef QDOT_P1_EVICT_NORMAL
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
     asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(x + e0), "r"(TILE * 8), "l"(pol)
                  : "memory");
     if (!NORM)
