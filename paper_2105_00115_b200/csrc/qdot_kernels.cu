@@ -932,6 +932,9 @@ static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, i
         case 6: return launch_pass1_t<NORM, VEC, 4, false, 7>(x, y, n, A, B, prm, st);
         case 7: return launch_pass1_t<NORM, VEC, 2, false, 6>(x, y, n, A, B, prm, st);
         case 8: return launch_pass1_t<NORM, VEC, 2, false, 10>(x, y, n, A, B, prm, st);
+        case 9: return launch_pass1_t<NORM, VEC, 4, true, 3>(x, y, n, A, B, prm, st);    // registers + L2
+        case 10: return launch_pass1_t<NORM, VEC, 2, true, 3>(x, y, n, A, B, prm, st);
+        case 11: return launch_pass1_t<NORM, VEC, 2, true, 6>(x, y, n, A, B, prm, st);
         default: break;
     }
 #endif

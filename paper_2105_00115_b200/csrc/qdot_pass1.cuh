@@ -437,9 +437,16 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
         double xa[EPT], ya[EPT], xb[EPT], yb[EPT];
         bool fa = false, fb = false;
         int64_t t = blockIdx.x;
+        if (L2D > 0 && tid == 0) {
+            for (int d = 2; d <= L2D + 1; ++d) p1_prefetch_l2<NORM>(x, y, n, blockIdx.x + d * stride, TILE);
+        }
         if (t < ntiles) p1_load<NORM, VEC, V>(x, y, n, t, tid, xa, ya, fa);
         while (t < ntiles) {
             const int64_t tb = t + stride;
+            if (L2D > 0 && tid == 0) {
+                p1_prefetch_l2<NORM>(x, y, n, t + (L2D + 2) * stride, TILE);
+                p1_prefetch_l2<NORM>(x, y, n, t + (L2D + 3) * stride, TILE);
+            }
             if (tb < ntiles) p1_load<NORM, VEC, V>(x, y, n, tb, tid, xb, yb, fb);
             p1_tile<FULL, QUEUE, V, WW>(S, my, kbias, A, B, xa, ya, t * TILE, n, fa, tid, qn, zc, nf);
             if (++since == FLUSH) { flush(); since = 0; }

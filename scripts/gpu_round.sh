@@ -19,6 +19,12 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ex
    -o gpurun_out/exact_$TAG python scripts/exact_time.py > gpurun_out/ncu_exact_$TAG.log 2>&1
 timeout 300 python scripts/exact_time.py > gpurun_out/exact_time_$TAG.json 2>&1
 timeout 300 python scripts/latency.py > gpurun_out/latency_$TAG.jsonl 2>&1
+timeout 300 python scripts/solver_bench.py > gpurun_out/solver_bench_$TAG.jsonl 2>&1
+timeout 300 python scripts/spmv_time.py > gpurun_out/spmv_time_$TAG.jsonl 2>&1
+timeout 300 python scripts/sustained_probe.py > gpurun_out/sustained_probe_$TAG.jsonl 2>&1
+( for n in 10000 1000000 268435456; do timeout 120 python scripts/step_graph_time.py $n; done ) > gpurun_out/step_graph_$TAG.jsonl 2>&1
+timeout 600 compute-sanitizer --tool memcheck python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/memcheck_smoke_$TAG.log 2>&1
+timeout 600 bash scripts/check_multirank.sh > gpurun_out/multirank_$TAG.log 2>&1
 # summarise every capture here (ncu is on the box) and keep only the reports named in KEEP
 # (gpurun copies back at most 64 MiB)
 for rep in pass1 batched c3pass1 exact; do
