@@ -850,7 +850,11 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned bl
     lc.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    // eager launches only: inside a CUDA graph capture the programmatic edges
+    // measured no gain (graph replay already removes the launch gaps)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (pdl_enabled()) cudaStreamIsCapturing(st, &cap);
+    at[0].val.programmaticStreamSerializationAllowed = (pdl_enabled() && cap == cudaStreamCaptureStatusNone) ? 1 : 0;
     lc.attrs = at;
     lc.numAttrs = 1;
     return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
