@@ -473,7 +473,7 @@ def main():
             "value_check": value_check,
             "pass1_modes": pass1_modes,
             "clocks": clocks,
-            "gpu_launches": (3 if world == 1 else 4) * args.steps,   # pass1, score, pass2 (+ finalize at N > 1)
+            "gpu_launches": (4 if world == 1 else 5) * args.steps,   # begin, pass1, score, pass2 (+ finalize at N > 1)
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
