@@ -111,6 +111,37 @@ class _DotReport:
 
 
 # --------------------------------------------------------------------------- matrices
+def sell_layout(torch, indptr, indices, data, n):
+    """CSR -> sliced ELL on the tensors' device: slices of 32 rows, entry j of
+    row r at slice_off[r // 32] + 32 j + r % 32 (a warp's 32 rows read one
+    coalesced line per j).  Returns (slice_off int64[ns], row_len int32[n],
+    cols int32[total], vals f64[total]) or None (no rows or entries, n >= 2^31,
+    or padding above 2x).  The order of a row's entries is kept, so a
+    sequential per-row sum equals scipy's csr_matvec."""
+    nnz = int(indptr[-1]) if n else 0
+    if n == 0 or nnz == 0 or n > (1 << 31) - 1:
+        return None
+    device = indptr.device
+    row_len = (indptr[1:] - indptr[:-1]).to(torch.int32)
+    ns = (n + 31) // 32
+    padded = torch.zeros(ns * 32, dtype=torch.int32, device=device)
+    padded[:n] = row_len
+    width = padded.view(ns, 32).max(dim=1).values.to(torch.int64)
+    slice_off = torch.zeros(ns + 1, dtype=torch.int64, device=device)
+    slice_off[1:] = torch.cumsum(width * 32, 0)
+    total = int(slice_off[-1])
+    if total > 2 * nnz + 32 * ns:
+        return None
+    rows = torch.repeat_interleave(torch.arange(n, device=device), row_len.to(torch.int64))
+    j = torch.arange(rows.numel(), device=device) - indptr[rows]
+    dest = slice_off[rows // 32] + 32 * j + rows % 32
+    cols = torch.zeros(total, dtype=torch.int32, device=device)
+    vals = torch.zeros(total, dtype=torch.float64, device=device)
+    cols[dest] = indices.to(torch.int32)
+    vals[dest] = data
+    return slice_off[:-1].contiguous(), row_len.contiguous(), cols, vals
+
+
 @dataclass
 class SparseMatrix:
     """CSR storage plus the symmetry promise the solvers rely on (apps.py:33-58);
@@ -154,31 +185,9 @@ class SparseMatrix:
         built on the device from the CSR arrays; None when a column index does
         not fit int32 or the padding would more than double the storage."""
         if self._sell is None:
-            torch, device = _dev()
+            torch, _ = _dev()
             indptr, indices, _, data = self.device_arrays()
-            n = self.n
-            if n == 0 or self.indices.size == 0 or self.n > (1 << 31) - 1:
-                self._sell = False
-                return None
-            row_len = (indptr[1:] - indptr[:-1]).to(torch.int32)
-            ns = (n + 31) // 32
-            padded = torch.zeros(ns * 32, dtype=torch.int32, device=device)
-            padded[:n] = row_len
-            width = padded.view(ns, 32).max(dim=1).values.to(torch.int64)
-            slice_off = torch.zeros(ns + 1, dtype=torch.int64, device=device)
-            slice_off[1:] = torch.cumsum(width * 32, 0)
-            total = int(slice_off[-1])
-            if total > 2 * int(indptr[-1]) + 32 * ns:
-                self._sell = False
-                return None
-            rows = torch.repeat_interleave(torch.arange(n, device=device), row_len.to(torch.int64))
-            j = torch.arange(rows.numel(), device=device) - indptr[rows]
-            dest = slice_off[rows // 32] + 32 * j + rows % 32
-            cols = torch.zeros(total, dtype=torch.int32, device=device)
-            vals = torch.zeros(total, dtype=torch.float64, device=device)
-            cols[dest] = indices.to(torch.int32)
-            vals[dest] = data
-            self._sell = (slice_off[:-1].contiguous(), row_len.contiguous(), cols, vals)
+            self._sell = sell_layout(torch, indptr, indices, data, self.n) or False
         return self._sell or None
 
     def matvec_device(self, xd, out=None):
