@@ -18,6 +18,7 @@ st = thread_state(x.device)
 ws = st.ws_ptr
 s = torch.cuda.current_stream().cuda_stream
 c = config_struct(Q.ToleranceConfig(1e-8), Q.ExactBinning())
+c.reserved = int(os.environ.get("P1MODE", "0"))      # pass-1 mode knob (qdot_b200_pass1), 0 = auto
 out = torch.zeros(1, dtype=torch.float64, device="cuda")
 
 
