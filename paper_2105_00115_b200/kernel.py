@@ -149,18 +149,33 @@ def _bin_rows(cbins, n_bins: int) -> np.ndarray:
     return np.frombuffer(cbins, dtype=_BIN_DTYPE, count=n_bins).copy()
 
 
-def _bound_terms(rows: np.ndarray, shift: int) -> np.ndarray:
+_EPS_LIST = [float(e) for e in _EPS_OF_CODE]
+_SMALL_TABLE = 256          # bin tables up to this size: scalar math (numpy's per-call cost dominates)
+
+
+def _bound_terms(rows: np.ndarray, shift: int):
     """M * ldexp(eps, upper - shift + 1) per bin, rounded exactly like the
     scalar terms of scoring.py:171-178 (ldexp first, then the product).  An
-    overflowing ldexp falls back to math.ldexp, which raises OverflowError
-    like the reference."""
+    overflowing ldexp raises OverflowError like the reference's math.ldexp.
+    Returns a list of floats."""
+    if rows.size <= _SMALL_TABLE:
+        return [float(c) * math.ldexp(_EPS_LIST[p], u - shift + 1)
+                for c, p, u in zip(rows["cardinality"].tolist(), rows["precision"].tolist(), rows["upper"].tolist())]
     eps = _EPS_OF_CODE[rows["precision"]]
     k = rows["upper"] - shift + 1
     with np.errstate(over="ignore"):
         p2 = np.ldexp(eps, np.clip(k, -4000, 4000))
     if not np.all(np.isfinite(p2)):
         p2 = np.array([math.ldexp(float(e), int(kk)) for e, kk in zip(eps, k)])
-    return rows["cardinality"].astype(np.float64) * p2
+    return (rows["cardinality"].astype(np.float64) * p2).tolist()
+
+
+def _plain_sum(terms) -> float:
+    """Left-to-right sum from 0.0 (scoring.py:195-199)."""
+    acc = 0.0
+    for t in terms:
+        acc += t
+    return acc
 
 
 def _make_bin_objects(rows: np.ndarray, indexer):
@@ -179,10 +194,10 @@ def _build_params(res, cbins, cfg, strategy, indexer, rows=None) -> ParameterSet
                       early_terminated=bool(res.early_terminated), n=int(res.n), eps_eff=float(res.eps_eff),
                       n_bins=int(res.n_bins), zero_count=int(res.zero_count), _indexer=indexer,
                       _make_bins=_make_bin_objects(rows, indexer))
-    # ParameterSet.rel_bound: plain left-to-right sum from 0.0 (scoring.py:195-199);
-    # np.add.accumulate is sequential, and the terms are >= 0
+    # ParameterSet.rel_bound: plain left-to-right sum from 0.0 (scoring.py:195-199)
     rel = _bound_terms(rows, int(res.e_max))
-    ps.rel_bound = float(np.add.accumulate(rel)[-1]) if rel.size else 0.0
+    ps.rel_bound = _plain_sum(rel)
+    ps._rel_terms = rel
     return ps
 
 
@@ -230,8 +245,8 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
     """Host-side report assembly (kernel.py:205-240)."""
     rows = _bin_rows(cbins, int(res.n_bins))
     params = _build_params(res, cbins, cfg, strategy, indexer, rows)
-    abs_bound = math.fsum(_bound_terms(rows, 0).tolist())
-    rel_bound = math.fsum(_bound_terms(rows, params.e_max).tolist())
+    abs_bound = math.fsum(_bound_terms(rows, 0))
+    rel_bound = math.fsum(params._rel_terms)
     rel_hypothesis = "assumed"
     rel_bound_e = None
     if is_norm:
@@ -243,7 +258,7 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
         else:
             holds = params.e_max <= fe or rows.size == 0
             rel_hypothesis = "holds" if (holds or is_norm) else "violated"
-            rel_bound_e = math.fsum(_bound_terms(rows, int(fe)).tolist())
+            rel_bound_e = math.fsum(_bound_terms(rows, int(fe)))
     counts = {level: 0 for level in PrecisionLevel}
     for i, level in enumerate((PrecisionLevel.PERFORATE, PrecisionLevel.HALF, PrecisionLevel.SINGLE,
                                PrecisionLevel.DOUBLE)):
