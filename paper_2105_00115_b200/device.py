@@ -27,10 +27,16 @@ def _torch():
     return torch
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
+    global _CUDA_OK
     torch = _torch()
-    if not torch.cuda.is_available():
-        raise RuntimeError("qdot_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    if not _CUDA_OK:                      # a success is cached; a failure raises every time
+        if not torch.cuda.is_available():
+            raise RuntimeError("qdot_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+        _CUDA_OK = True
     return torch
 
 
