@@ -220,6 +220,40 @@ def measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, norm, Q, config_
     del X, Y, vals, cnt, info
     torch.cuda.empty_cache()
 
+    # the same C2 inputs under the other split mode (benchmark
+    # both, headline the qdot() default) and in norm mode (x . x: one vector
+    # read, the solvers' r . r), whole single-device step each
+    from paper_2105_00115_b200.device import thread_state
+    st = thread_state(dev)
+    ws = st.ws_ptr
+
+    def whole_step(xp, yp, m, nm, cfg_c):
+        def one():
+            _lib.check(lib.qdot_b200_begin(ws, s), lib)
+            _lib.check(lib.qdot_b200_pass1(xp, yp, m, nm, ctypes.byref(cfg_c), m, ws, s), lib)
+            _lib.check(lib.qdot_b200_score_finalize(ws, m, ctypes.byref(cfg_c), s), lib)
+            _lib.check(lib.qdot_b200_pass2_finalize(xp, yp, m, nm, ws, s), lib)
+        for _ in range(3):
+            one()
+        e0.record(stream)
+        for _ in range(reps):
+            one()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
+        return e0.elapsed_time(e1) / reps, float(st.result.value)
+
+    if not norm:
+        pb = config_struct(Q.ToleranceConfig(1e-8, Q.SplitMode.PER_BIN), Q.ExactBinning())
+        ms_pb, v_pb = whole_step(xd.data_ptr(), yd.data_ptr(), n, 0, pb)
+        res["c2_split_per_bin"] = {"workload": "C2 inputs, eps 1e-8, split=per-bin, exact, whole qdot step",
+                                   "ms": ms_pb, "elements_per_s": n / (ms_pb * 1e-3), "value": v_pb}
+        nc = config_struct(Q.ToleranceConfig(1e-8), Q.ExactBinning())
+        ms_nm, v_nm = whole_step(xd.data_ptr(), xd.data_ptr(), n, 1, nc)
+        res["c2_norm"] = {"workload": "C2 x vector, x . x (norm mode: 8 B/element), eps 1e-8, exact, whole qdot step",
+                          "ms": ms_nm, "elements_per_s": n / (ms_nm * 1e-3), "GBps": n * 8 / (ms_nm * 1e-3) / 1e9,
+                          "value": v_nm}
+
     # BASELINE configs[2] (C3): the ill-conditioned distribution of SURVEY.md §8d
     # (cond ~1e12, exponent sums spanning +-300), generated on the device with
     # torch (same law as oracle.gen_illcond, other bits), eps 1e-12, whole step
@@ -241,9 +275,6 @@ def measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, norm, Q, config_
     yc = torch.cat([y1, -y1 * (1.0 + delta)])[perm].contiguous()
     del a, b, sgn, x1, y1, delta, perm
     c3 = config_struct(Q.ToleranceConfig(1e-12), Q.ExactBinning())
-    from paper_2105_00115_b200.device import thread_state
-    st = thread_state(dev)
-    ws = st.ws_ptr
     m = 2 * h
 
     def c3_step():
