@@ -423,3 +423,34 @@ def test_pass2_finalize_sequences_agree(strategy, eps, n):
             assert abs(outs[0][0] - ref.value) <= ref.abs_cap
         else:
             assert outs[0][0] == ref.value
+
+
+@pytest.mark.parametrize("n", [5000, 1 << 17, (1 << 22) + 3])
+def test_inputs_written_just_before_the_call_are_seen(n):
+    """The launch chain (k_begin launched normally, then pass 1 / score /
+    pass 2 with programmatic dependent launch) is ordered after a kernel that
+    rewrites x and y on the same stream with no host sync in between: each
+    call must see the new data (eager launches and the cached graph path)."""
+    def agree(rep, ref):
+        # a HALF bin the reference sums order-sensitively in fp32: its budget applies
+        return abs(rep.value - ref.value) <= ref.abs_cap if rep.half_order_sensitive else rep.value == ref.value
+
+    rng = np.random.default_rng(n)
+    xs = [rng.standard_normal(n) * np.exp2(rng.integers(-20, 20, n)) for _ in range(4)]
+    ys = [rng.standard_normal(n) for _ in range(4)]
+    want = [O.qdot(a, b, 1e-8) for a, b in zip(xs, ys)]
+    xsrc = [torch.from_numpy(a).cuda() for a in xs]
+    ysrc = [torch.from_numpy(b).cuda() for b in ys]
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    cfg = Q.ToleranceConfig(1e-8)
+    torch.cuda.synchronize()
+    for rep in range(3):                       # the third round runs through the cached graph
+        for i in range(4):
+            x.copy_(xsrc[i])                   # device kernels on the current stream, no sync
+            y.copy_(ysrc[i])
+            assert agree(Q.qdot(x, y, cfg), want[i]), (rep, i)
+    # norm mode on a vector rewritten in place
+    for i in range(2):
+        x.copy_(xsrc[i])
+        assert agree(Q.qdot(x, x, cfg), O.qdot(xs[i], xs[i], 1e-8)), i
