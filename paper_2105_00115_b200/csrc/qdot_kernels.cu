@@ -1,5 +1,7 @@
 // qdot_kernels.cu -- sm_100a kernels of the qdot hot path.
 //
+//   begin     zero the exchange regions and rank-local counters (a normal
+//             launch: it orders the call after any kernel that wrote x, y)
 //   pass1     streaming pass over x, y (16 B/elem, 8 B/elem in norm mode):
 //             exponent extraction, exact exponent-sum histogram, exact per-key
 //             DOUBLE partials and exact-binning HALF/SINGLE partials
@@ -8,11 +10,16 @@
 //             emulate.py:116-154 bin_dot work).
 //   score     one CTA: partition + bin scores + precisions + LUT from the
 //             histogram alone (kernel.py:59-72, binning.py:191-284,
-//             scoring.py:96-216).
+//             scoring.py:96-216); single-device calls also finalize here when
+//             no pass 2 follows, from key rows staged in shared memory.
 //   pass2     second streaming pass, only when a HALF/SINGLE bin has upper
-//             u != e for some member key (ranged / split / early bins).
+//             u != e for some member key (ranged / split / early bins); on a
+//             single device its last CTA finalizes.
 //   finalize  one CTA: per-bin exact sums rounded like the reference, and the
-//             ascending-upper Neumaier fold (emulate.py:154-163).
+//             ascending-upper Neumaier fold (emulate.py:154-163); a separate
+//             launch only after the multi-GPU allreduce of region B.
+//   pass1, score and pass2 are launched with programmatic dependent launch
+//   (eager launches; each waits in griddepcontrol.wait before the workspace).
 //   bin_ids   lazy Bin.indices support (binning.py:174).
 //
 // No tensor cores: this is a memory-bound integer/bit reduction.
