@@ -1,0 +1,49 @@
+"""bench.py's driver contract, checked on CPU: the reference arm (the C oracle
+port on the host cores) prints one JSON line with the contract's keys, the
+BASELINE.json metric, and a cpu_baseline / e2e block describing the run; the
+B200 arm refuses to run without a GPU instead of falling back to the CPU."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args, timeout=300):
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT, capture_output=True,
+                          text=True, timeout=timeout)
+
+
+def test_reference_arm_json_line():
+    p = _run("--impl", "reference", "--steps", "2", "--warmup", "1", "--cpu-sample", str(1 << 16))
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        base = json.load(f)
+    assert d["impl"] == "reference"
+    assert d["metric"] == base["metric"]
+    for k in ("value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["value"] > 0 and d["unit"] == "elements/s" and d["higher_is_better"] is True
+    assert d["n_gpus"] == 1 and d["steps"] == 2
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
+    assert cb["sample"]
+    e = d["e2e"]
+    assert e["value"] == d["value"] and e["unit"] == d["unit"]
+    assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_b200_arm_fails_loudly_without_a_gpu():
+    p = _run("--steps", "3", "--warmup", "3", "--elements", "4096", "--no-secondary", "--e2e-steps", "0",
+             "--no-cpu-baseline")
+    assert p.returncode != 0
+    assert not [ln for ln in p.stdout.splitlines() if ln.startswith("{") and '"value"' in ln]
