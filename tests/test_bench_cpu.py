@@ -47,3 +47,16 @@ def test_b200_arm_fails_loudly_without_a_gpu():
              "--no-cpu-baseline")
     assert p.returncode != 0
     assert not [ln for ln in p.stdout.splitlines() if ln.startswith("{") and '"value"' in ln]
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    """N > 1 (launched like the driver does): rank 0 alone runs and prints."""
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29617", os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1",
+                        "--cpu-sample", str(1 << 15)], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
