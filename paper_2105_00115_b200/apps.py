@@ -31,6 +31,7 @@ from __future__ import annotations
 import csv
 import ctypes
 import math
+import threading
 from dataclasses import dataclass, field
 from typing import IO, List, Optional, Tuple, Union
 
@@ -38,7 +39,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _lib
-from .binning import ExactBinning, Strategy
+from .binning import ExactBinning, Strategy, strategy_label
 from .device import config_struct, require_cuda, stream_handle, thread_state
 from .kernel import _raise_status, run_device
 from .scoring import LEVELS_ASC, PrecisionLevel, SplitMode, ToleranceConfig
@@ -156,6 +157,9 @@ class SparseMatrix:
     _csr: Optional[sp.csr_matrix] = field(default=None, repr=False, compare=False)
     _device: Optional[tuple] = field(default=None, repr=False, compare=False)
     _sell: Optional[object] = field(default=None, repr=False, compare=False)
+    # captured solver-iteration graphs and the device vectors they read, per
+    # solver configuration (see _graph_entry)
+    _graphs: dict = field(default_factory=dict, repr=False, compare=False)
 
     @classmethod
     def from_csr(cls, m: sp.csr_matrix, symmetric: bool = True) -> "SparseMatrix":
@@ -319,6 +323,29 @@ class PMResult:
 GRAPH_MIN = 2048          # solves of at least this many unknowns run each iteration as one CUDA graph
 
 
+class _GraphEntry:
+    """A solver's captured iteration graph(s) and the device vectors they
+    read, kept on the matrix so a repeated solve replays instead of
+    re-capturing (a capture costs ~2-3 ms).  One solve at a time holds it."""
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.G = None
+        self.graphs = None
+        self.bufs = None
+
+
+def _cfg_key(cfg: ToleranceConfig):
+    return (float(cfg.epsilon), cfg.split.value, int(cfg.input_mu))
+
+
+def _graph_entry(a: "SparseMatrix", key) -> Optional[_GraphEntry]:
+    """The entry for `key`, locked for this solve, or None when another solve
+    holds it (that solve then uses fresh buffers and its own capture)."""
+    e = a._graphs.setdefault(key, _GraphEntry())
+    return e if e.lock.acquire(blocking=False) else None
+
+
 class _IterGraph:
     """Device resources of graph-captured solver iterations: two qdot
     workspaces (one per dot product of an iteration), the scalar state st[8],
@@ -428,40 +455,65 @@ def acg(a: SparseMatrix, b, x0=None, tau: float = 1e-8, epsilon: float = 1e-8,
     cfg = ToleranceConfig(epsilon=epsilon, split=split)
     torch, device = _dev()
     n = a.n
+    use_graph = n >= GRAPH_MIN and max_iters > 0
+    entry = _graph_entry(a, ("acg", _cfg_key(cfg), strategy_label(strategy), str(device))) if use_graph else None
+    try:
+        return _acg(a, b, x0, tau, max_iters, cfg, strategy, torch, device, n, use_graph, entry)
+    finally:
+        if entry is not None:
+            entry.lock.release()
+
+
+def _acg(a, b, x0, tau, max_iters, cfg, strategy, torch, device, n, use_graph, entry) -> CGResult:
     dots = _Dots(cfg, strategy)
-    x = torch.zeros(n, dtype=torch.float64, device=device) if x0 is None else _to_device(x0, n).clone()
+    cached = entry is not None and entry.G is not None
+    if cached:                                                # the captured graph reads these buffers
+        x, r, p, q = entry.bufs
+        if x0 is None:
+            x.zero_()
+        else:
+            x.copy_(_to_device(x0, n))
+    else:
+        x = torch.zeros(n, dtype=torch.float64, device=device) if x0 is None else _to_device(x0, n).clone()
+        q = torch.empty(n, dtype=torch.float64, device=device)
+        r = torch.empty(n, dtype=torch.float64, device=device)
+        p = torch.empty(n, dtype=torch.float64, device=device)
     bd = _to_device(b, n)
     trace = SolveTrace()
 
-    q = a.matvec_device(x)
-    r = torch.empty_like(bd)
+    a.matvec_device(x, out=q)
     _update(_SUB, bd, 1.0, q, r)                              # r = b - A x (1.0 * q is exact)
-    p = r.clone()
+    p.copy_(r)
     c_rep = _norm_dot(dots, r)
     c = c_rep.value
     resid = math.sqrt(c)
     trace.record(0, "rtr", c_rep, resid)
 
     k = 0
-    if n >= GRAPH_MIN and resid > tau and max_iters > 0:
+    if use_graph and resid > tau:
         # one CUDA graph per iteration: SpMV, p.Ap, alpha, x and r updates, r.r,
         # beta, p update, publish -- one host wake-up per iteration
-        G = _IterGraph(device)
+        if cached:
+            G, g = entry.G, entry.graphs
+        else:
+            G = _IterGraph(device)
+            cst = config_struct(cfg, strategy)
+
+            def body(stream):
+                a.matvec_device(p, out=q)
+                G.qdot_nodes(0, p, q, False, cst, stream)
+                G.scalar(0, 0, stream)                          # alpha = c / d
+                G.update(_ADD, x, 1, p, x, stream)              # x = x + alpha * p
+                G.update(_SUB, r, 1, q, r, stream)              # r = r - alpha * q
+                G.qdot_nodes(1, r, r, True, cst, stream)
+                G.scalar(1, 1, stream)                          # beta = c_new / c; c = c_new
+                G.update(_ADD, r, 2, p, p, stream)              # p = r + beta * p
+                G.publish(stream)
+
+            g = G.capture(body)
+            if entry is not None:
+                entry.G, entry.graphs, entry.bufs = G, g, (x, r, p, q)
         G.st[0] = c
-        cst = config_struct(cfg, strategy)
-
-        def body(stream):
-            a.matvec_device(p, out=q)
-            G.qdot_nodes(0, p, q, False, cst, stream)
-            G.scalar(0, 0, stream)                          # alpha = c / d
-            G.update(_ADD, x, 1, p, x, stream)              # x = x + alpha * p
-            G.update(_SUB, r, 1, q, r, stream)              # r = r - alpha * q
-            G.qdot_nodes(1, r, r, True, cst, stream)
-            G.scalar(1, 1, stream)                          # beta = c_new / c; c = c_new
-            G.update(_ADD, r, 2, p, p, stream)              # p = r + beta * p
-            G.publish(stream)
-
-        g = G.capture(body)
         while resid > tau and k < max_iters:
             r_pq, r_rr, st = G.run(g)
             d_rep = _dot_report(r_pq)
@@ -507,38 +559,57 @@ def apm(a: SparseMatrix, x0, tau: float = 1e-6, epsilon: float = 1e-7, split: Sp
     nrm = float(np.linalg.norm(x_h))                          # host, as apps.py:292
     if nrm == 0.0:
         raise ZeroIterateError("x0 is the zero vector")
-    x = _to_device(x_h / nrm, a.n)
-    torch, _ = _dev()
+    torch, device = _dev()
+    use_graph = a.n >= GRAPH_MIN and max_iters > 0
+    entry = _graph_entry(a, ("apm", _cfg_key(cfg), strategy_label(strategy), str(device))) if use_graph else None
+    try:
+        return _apm(a, x_h, nrm, tau, max_iters, cfg, strategy, torch, device, use_graph, entry)
+    finally:
+        if entry is not None:
+            entry.lock.release()
+
+
+def _apm(a, x_h, nrm, tau, max_iters, cfg, strategy, torch, device, use_graph, entry) -> PMResult:
+    cached = entry is not None and entry.G is not None
+    if cached:                                                # the captured graphs read these buffers
+        x, x_next, z = entry.bufs
+        x.copy_(_to_device(x_h / nrm, a.n))
+    else:
+        x = _to_device(x_h / nrm, a.n).clone()
+        z = torch.empty_like(x)
+        x_next = torch.empty_like(x)
     dots = _Dots(cfg, strategy)
     trace = SolveTrace()
-    z = torch.empty_like(x)
-    x_next = torch.empty_like(x)
 
     lam_prev = None
     lam = 0.0
     k = 0
     converged = False
-    if a.n >= GRAPH_MIN and max_iters > 0:
+    if use_graph:
         # two CUDA graphs (the x / x_next buffers swap roles every iteration):
         # SpMV, z.z, s = sqrt(z.z), x_next = z / s, x.x_next, publish
-        _, device = _dev()
-        G = _IterGraph(device)
-        cst = config_struct(cfg, strategy)
         bufs = (x, x_next)
+        if cached:
+            G, graphs = entry.G, entry.graphs
+        else:
+            G = _IterGraph(device)
+            cst = config_struct(cfg, strategy)
 
-        def body_for(cur, nxt):
-            def body(stream):
-                a.matvec_device(cur, out=z)
-                G.qdot_nodes(0, z, z, True, cst, stream)
-                G.scalar(2, 0, stream)                      # st[0] = z.z, st[3] = sqrt(z.z)
-                G.update(_DIV, z, 3, None, nxt, stream)     # x_next = z / s
-                G.qdot_nodes(1, cur, nxt, False, cst, stream)
-                G.publish(stream)
-            return body
+            def body_for(cur, nxt):
+                def body(stream):
+                    a.matvec_device(cur, out=z)
+                    G.qdot_nodes(0, z, z, True, cst, stream)
+                    G.scalar(2, 0, stream)                      # st[0] = z.z, st[3] = sqrt(z.z)
+                    G.update(_DIV, z, 3, None, nxt, stream)     # x_next = z / s
+                    G.qdot_nodes(1, cur, nxt, False, cst, stream)
+                    G.publish(stream)
+                return body
 
-        a.device_arrays()                                   # host->device copies cannot be captured
-        a.sell_arrays()
-        graphs = [G.capture(body_for(bufs[0], bufs[1])), G.capture(body_for(bufs[1], bufs[0]))]
+            a.device_arrays()                                   # host->device copies cannot be captured
+            a.sell_arrays()
+            graphs = [G.capture(body_for(bufs[0], bufs[1])), G.capture(body_for(bufs[1], bufs[0]))]
+            if entry is not None:
+                entry.G, entry.graphs, entry.bufs = G, graphs, (x, x_next, z)
         while k < max_iters:
             r_zz, r_lam, _st = G.run(graphs[k % 2])
             c_rep = _dot_report(r_zz)

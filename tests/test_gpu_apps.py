@@ -183,3 +183,44 @@ def test_large_stencil_runs_on_device():
     res = apps.acg(a, b, tau=1e-6, epsilon=1e-8)
     assert res.converged and math.isfinite(res.residual_norm)
     assert np.abs(res.x - 1.0).max() < 1e-6
+
+
+def _same_cg(r1, r2):
+    return (r1.iterations == r2.iterations and r1.x.tobytes() == r2.x.tobytes()
+            and float(r1.residual_norm).hex() == float(r2.residual_norm).hex() and rows(r1.trace) == rows(r2.trace))
+
+
+def test_repeated_solves_replay_the_cached_graph():
+    """A second solve on the same matrix replays the captured iteration graph
+    with new b / x0 (and new start vectors for APM): every result equals a
+    solve on a fresh matrix object, also with two threads solving at once."""
+    import threading
+    a, b = apps.gen_stencil(16, 16, 12)                   # n = 3072 >= GRAPH_MIN
+    rng = np.random.default_rng(9)
+    rhs = [b, rng.standard_normal(a.n), rng.standard_normal(a.n)]
+    x0s = [None, None, rng.standard_normal(a.n)]
+    fresh = [apps.acg(apps.SparseMatrix.from_csr(a.csr()), bb, x0=xx, tau=1e-8, epsilon=1e-8)
+             for bb, xx in zip(rhs, x0s)]
+    for _ in range(2):
+        for bb, xx, want in zip(rhs, x0s, fresh):
+            assert _same_cg(apps.acg(a, bb, x0=xx, tau=1e-8, epsilon=1e-8), want)
+    out = [None, None]
+
+    def solve(i):
+        out[i] = apps.acg(a, rhs[i + 1], x0=x0s[i + 1], tau=1e-8, epsilon=1e-8)
+    ts = [threading.Thread(target=solve, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert _same_cg(out[0], fresh[1]) and _same_cg(out[1], fresh[2])
+
+    lap = apps.gen_graph_laplacian(3000, 0.003, seed=5)
+    starts = [rng.standard_normal(lap.n) for _ in range(3)]
+    pf = [apps.apm(apps.SparseMatrix.from_csr(lap.csr()), s0, tau=1e-6, epsilon=1e-7, max_iters=60) for s0 in starts]
+    for _ in range(2):
+        for s0, want in zip(starts, pf):
+            got = apps.apm(lap, s0, tau=1e-6, epsilon=1e-7, max_iters=60)
+            assert got.iterations == want.iterations and got.x.tobytes() == want.x.tobytes()
+            assert float(got.eigenvalue).hex() == float(want.eigenvalue).hex()
+            assert rows(got.trace) == rows(want.trace)
