@@ -321,6 +321,8 @@ class PMResult:
 
 # --------------------------------------------------------------------------- graph iterations
 GRAPH_MIN = 2048          # solves of at least this many unknowns run each iteration as one CUDA graph
+GRAPH_REPEAT = True       # smaller ones too from their second solve on the same matrix and configuration
+                          # (a capture costs ~2-3 ms: worth it once the graph is replayed by later solves)
 
 
 class _GraphEntry:
@@ -330,6 +332,7 @@ class _GraphEntry:
 
     def __init__(self):
         self.lock = threading.Lock()
+        self.solves = 0
         self.G = None
         self.graphs = None
         self.bufs = None
@@ -455,12 +458,13 @@ def acg(a: SparseMatrix, b, x0=None, tau: float = 1e-8, epsilon: float = 1e-8,
     cfg = ToleranceConfig(epsilon=epsilon, split=split)
     torch, device = _dev()
     n = a.n
-    use_graph = n >= GRAPH_MIN and max_iters > 0
-    entry = _graph_entry(a, ("acg", _cfg_key(cfg), strategy_label(strategy), str(device))) if use_graph else None
+    entry = _graph_entry(a, ("acg", _cfg_key(cfg), strategy_label(strategy), str(device))) if max_iters > 0 else None
+    use_graph = max_iters > 0 and (n >= GRAPH_MIN or (GRAPH_REPEAT and entry is not None and entry.solves > 0))
     try:
         return _acg(a, b, x0, tau, max_iters, cfg, strategy, torch, device, n, use_graph, entry)
     finally:
         if entry is not None:
+            entry.solves += 1
             entry.lock.release()
 
 
@@ -560,12 +564,13 @@ def apm(a: SparseMatrix, x0, tau: float = 1e-6, epsilon: float = 1e-7, split: Sp
     if nrm == 0.0:
         raise ZeroIterateError("x0 is the zero vector")
     torch, device = _dev()
-    use_graph = a.n >= GRAPH_MIN and max_iters > 0
-    entry = _graph_entry(a, ("apm", _cfg_key(cfg), strategy_label(strategy), str(device))) if use_graph else None
+    entry = _graph_entry(a, ("apm", _cfg_key(cfg), strategy_label(strategy), str(device))) if max_iters > 0 else None
+    use_graph = max_iters > 0 and (a.n >= GRAPH_MIN or (GRAPH_REPEAT and entry is not None and entry.solves > 0))
     try:
         return _apm(a, x_h, nrm, tau, max_iters, cfg, strategy, torch, device, use_graph, entry)
     finally:
         if entry is not None:
+            entry.solves += 1
             entry.lock.release()
 
 

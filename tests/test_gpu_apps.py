@@ -46,6 +46,7 @@ def iteration_mode(request, monkeypatch):
         monkeypatch.setattr(apps, "GRAPH_MIN", 1)
     else:
         monkeypatch.setattr(apps, "GRAPH_MIN", 1 << 62)
+        monkeypatch.setattr(apps, "GRAPH_REPEAT", False)
     return request.param
 
 
@@ -214,6 +215,11 @@ def test_repeated_solves_replay_the_cached_graph():
     for t in ts:
         t.join()
     assert _same_cg(out[0], fresh[1]) and _same_cg(out[1], fresh[2])
+
+    small, sb = apps.gen_stencil(8, 8, 8)                   # n = 512 < GRAPH_MIN: eager, then a graph
+    sfresh = apps.acg(apps.SparseMatrix.from_csr(small.csr()), sb, tau=1e-8, epsilon=1e-8)
+    for _ in range(3):
+        assert _same_cg(apps.acg(small, sb, tau=1e-8, epsilon=1e-8), sfresh)
 
     lap = apps.gen_graph_laplacian(3000, 0.003, seed=5)
     starts = [rng.standard_normal(lap.n) for _ in range(3)]
