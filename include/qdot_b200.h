@@ -78,8 +78,9 @@ typedef struct {
     int32_t first_key;   /* first / last present exponent-sum key (e + 2148)       */
     int32_t last_key;
     int32_t flags;       /* bit0: HALF bin whose fp32 sequential sum in the
-                            reference is not provably exact (value then agrees
-                            within the bin budget, not necessarily bit-exact)     */
+                            reference is not provably exact (its order matters);
+                            bit1: that sum was replayed in index order by
+                            qdot_b200_half_ordered (value bit-exact again)        */
     double value;        /* per-bin value (already scaled by 2^upper)              */
 } qdot_bin;
 
@@ -96,7 +97,8 @@ typedef struct {
     int32_t e_min, e_max;    /* 0, 0 when degenerate                              */
     int32_t early_terminated;
     int32_t pass2_needed;    /* a second streaming pass was required              */
-    int32_t half_order_sensitive; /* any bin with flags bit0                      */
+    int32_t half_order_sensitive; /* 1: some bin has flags bit0 (value pending the
+                                     ordered replay); 2: replayed, value final    */
     int32_t select_ns;       /* device time: pass 1 start -> scoring done         */
     int32_t compute_ns;      /* device time: scoring done -> finalize done        */
     int32_t reserved[3];
@@ -193,6 +195,33 @@ int qdot_b200_batched(const double* X, const double* Y, int64_t rows, int64_t le
 int qdot_b200_bin_ids(const double* x, const double* y, int64_t n, int norm, const int32_t* lut_bin,
                       int32_t* bin_ids, void* stream);
 
+/* Stable counting-sort scatter: the members of every bin in ascending index
+ * order, i.e. the reference's `order` slices (binning.py:46-55, 88-116; the
+ * np.sort of ranged / split members, binning.py:218, 270) and zero_idx
+ * (floatbits.py:74-76).  Slot 0 = exact-zero products, slot 1 + b = bin b
+ * (lut_bin: exponent-sum key -> bin id).  want[slot] != 0 selects the slots
+ * written (NULL: all).  Outputs: bin_start[n_bins + 2] (device int64: start
+ * of each slot in `order`, bin_start[n_bins + 1] = total) and the indices.
+ * scratch: device memory of qdot_b200_order_scratch_bytes(n, n_bins). */
+size_t qdot_b200_order_scratch_bytes(int64_t n, int32_t n_bins);
+int qdot_b200_bin_order(const double* x, const double* y, int64_t n, int norm, const int32_t* lut_bin,
+                        int32_t n_bins, const uint8_t* want, int64_t* bin_start, int64_t* order, void* scratch,
+                        size_t scratch_bytes, void* stream);
+/* HALF bins the finalize flagged order-sensitive (qdot_bin.flags bit 0):
+ * replay the reference's sequential fp32 sum in index order (emulate.py:150-151)
+ * after the pipeline, on the workspace of that call.  stage bits: 1 = member
+ * order of the flagged bins into `order` (order_len >= their total
+ * cardinality) and zero start values; 2 = the fp32 chains from the start
+ * values; 4 = rescale those bins (math.ldexp semantics, bin flags |= 2) and
+ * re-fold the result (emulate.py:154-163; result.half_order_sensitive = 2).
+ * chain: device float[n_bins], the running fp32 sum per bin (stage 1 zeroes
+ * it, stage 2 continues from it, stage 4 reads it).  One device: stage 7.
+ * Contiguous shards: 1, then 2 on every rank in rank order with the previous
+ * rank's chain copied in, then 4 everywhere with the last rank's chain. */
+int qdot_b200_half_ordered(const double* x, const double* y, int64_t n, int norm, void* ws, int32_t n_bins,
+                           int64_t* order, int64_t order_len, float* chain, void* scratch, size_t scratch_bytes,
+                           int stage, void* stream);
+
 /* --- solver callers (apps.py: acg / apm) -------------------------------------- */
 /* y = A x for a CSR matrix (int64 indptr[n_rows+1], int32 or int64 column
  * indices: index_bytes 4 or 8).  Each row is summed sequentially from +0.0 in
@@ -253,6 +282,16 @@ int qdot_b200_exact_accumulate(const double* x, const double* y, int64_t n, int 
 int qdot_b200_exact_plain(const double* x, const double* y, int64_t n, int norm, void* xws, void* stream);
 int qdot_b200_exact_finalize(void* xws, void* stream);
 int qdot_b200_exact_fetch(const void* xws, qdot_exact_result* out, void* stream);
+
+/* --- synthetic inputs on the device (bench / harness at 2^28-2^31) ----------- */
+/* x[i], y[i] (y may be NULL) for global indices offset..offset+n-1 of one
+ * vector pair: a pure function of (law, param, seed, index), so shards of any
+ * rank count concatenate to the unsharded vectors.  Laws: 0 standard normal
+ * (SURVEY.md §8d C1/C2/C4/C5), 1 ill-conditioned pairs (C3), 2 / 3 harness
+ * families A / B with spread param = t (harness.py:61-76).  Same laws as the
+ * numpy generators, not their bytes. */
+int qdot_b200_generate(int law, double param, uint64_t seed, int64_t offset, int64_t n, double* x, double* y,
+                       void* stream);
 
 /* --- measurement ------------------------------------------------------------- */
 /* stream n doubles (16-byte aligned) once with pass 1's load pattern and

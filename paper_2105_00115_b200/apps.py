@@ -213,6 +213,16 @@ class SparseMatrix:
                                           xd.data_ptr(), out.data_ptr(), stream_handle(xd.device)), lib)
         return out
 
+    def clear_graphs(self) -> None:
+        """Drop the cached solver-iteration graphs and their device buffers
+        (entries a running solve holds are kept)."""
+        with _graphs_lock:
+            for k in list(self._graphs):
+                e = self._graphs[k]
+                if e.lock.acquire(blocking=False):
+                    del self._graphs[k]
+                    e.lock.release()
+
     def matvec(self, v):
         """A v on the device; numpy in -> numpy out, tensor in -> tensor out."""
         torch, _ = _dev()
@@ -342,10 +352,26 @@ def _cfg_key(cfg: ToleranceConfig):
     return (float(cfg.epsilon), cfg.split.value, int(cfg.input_mu))
 
 
+GRAPH_CACHE_MAX = 4       # captured configurations kept per matrix (each holds two ~67 MB qdot workspaces)
+_graphs_lock = threading.Lock()
+
+
 def _graph_entry(a: "SparseMatrix", key) -> Optional[_GraphEntry]:
     """The entry for `key`, locked for this solve, or None when another solve
-    holds it (that solve then uses fresh buffers and its own capture)."""
-    e = a._graphs.setdefault(key, _GraphEntry())
+    holds it (that solve then uses fresh buffers and its own capture).  The
+    per-matrix cache is an LRU of GRAPH_CACHE_MAX entries: the least recently
+    used entry that no solve holds is dropped (with its workspaces) first."""
+    with _graphs_lock:
+        e = a._graphs.pop(key, None) or _GraphEntry()
+        a._graphs[key] = e                                    # most recently used last
+        if len(a._graphs) > GRAPH_CACHE_MAX:
+            for k in list(a._graphs):
+                if len(a._graphs) <= GRAPH_CACHE_MAX:
+                    break
+                old = a._graphs[k]
+                if k != key and old.lock.acquire(blocking=False):
+                    del a._graphs[k]
+                    old.lock.release()
     return e if e.lock.acquire(blocking=False) else None
 
 
@@ -406,7 +432,10 @@ class _IterGraph:
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            g.capture_begin()
+            # thread-local capture mode: another thread's solve or qdot call
+            # (allocations, stream queries, syncs) neither invalidates this
+            # capture nor fails because of it
+            g.capture_begin(capture_error_mode="thread_local")
             try:
                 body(side.cuda_stream)
             finally:

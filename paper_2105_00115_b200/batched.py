@@ -11,7 +11,9 @@ One warp per row streams the row once and finishes the whole pipeline in
 registers and shared memory (csrc/qdot_batched.cuh).  Rows the fused kernel
 flags QDOT_BATCH_GENERAL (non-exact strategies, exponents spread over more
 than 64 values, DOUBLE overflow, ...) are recomputed here through the
-single-vector device pipeline, so results never depend on that split.
+single-vector device pipeline, so results never depend on that split; so are
+rows with a HALF bin whose fp32 sequential sum is order-sensitive (that
+pipeline replays it in index order, qdot_b200_half_ordered).
 """
 
 from __future__ import annotations
@@ -99,7 +101,9 @@ def qdot_batched(X, Y, cfg: ToleranceConfig, strategy: Strategy = None) -> Batch
     st = inf[:, 3]
     if np.any(st & NONFINITE):
         raise ValueError("inputs must be finite")                       # floatbits.py:70-71
-    general = np.flatnonzero(st & GENERAL)
+    # rows with a HALF bin the reference sums order-sensitively are redone by
+    # the single-vector pipeline, which replays that fp32 sum in index order
+    general = np.flatnonzero(st & (GENERAL | HALF_ORDER))
     rep = BatchedReport(values=v.copy(), counts=cn.copy(), n_bins=inf[:, 0].copy(), e_min=inf[:, 1].copy(),
                         e_max=inf[:, 2].copy(), early_terminated=(st & EARLY) != 0,
                         half_order_sensitive=(st & HALF_ORDER) != 0, general_rows=general)

@@ -26,13 +26,7 @@ namespace {
 constexpr int T = 256;
 
 int grid_for(int64_t n, int per_thread) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (!sms) sms = 148;
-    }
+    const int sms = qd::device_sm_count();
     int64_t g = (n + (int64_t)T * per_thread - 1) / ((int64_t)T * per_thread);
     int64_t cap = (int64_t)sms * 8;
     if (g > cap) g = cap;
@@ -212,12 +206,7 @@ int qdot_b200_publish_iter(const void* ws_a, const void* ws_b, const double* st,
 int qdot_b200_read_probe(const double* x, int64_t n, double* out, void* stream) {
     if (n < 0 || (n > 0 && (!x || !out)) || (reinterpret_cast<uintptr_t>(x) & 15u)) return QDOT_ERR_ARG;
     if (n < 2) return QDOT_OK;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = qd::device_sm_count();
     k_read_probe<<<sms * 8, T, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const double2*>(x), n / 2, out);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "read_probe");

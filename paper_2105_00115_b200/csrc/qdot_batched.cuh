@@ -196,8 +196,8 @@ __device__ __forceinline__ void b_prefetch(const double* xr, const double* yr, c
         py = yn;
     }
     if (e0 + B_CHUNK > len) return;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(px + e0), "r"(B_CHUNK * 8) : "memory");
-    if (!norm) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(py + e0), "r"(B_CHUNK * 8) : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(bulk_aligned(px + e0)), "r"(B_CHUNK * 8) : "memory");
+    if (!norm) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(bulk_aligned(py + e0)), "r"(B_CHUNK * 8) : "memory");
 }
 
 // warp iteration: 128 elements, lane holds {2l, 2l+1, 64+2l, 65+2l}

@@ -29,6 +29,49 @@
 
 namespace qd {
 
+#ifdef __CUDACC__
+// ---- per-device launch facts ------------------------------------------------
+// Function attributes (the dynamic shared-memory opt-in), occupancy and the SM
+// count belong to a device context, so every cache of them is indexed by the
+// current device: one process may drive several GPUs.
+constexpr int MAX_DEVICES = 64;
+
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return (d >= 0 && d < MAX_DEVICES) ? d : 0;
+}
+
+inline int device_sm_count() {
+    static int sms[MAX_DEVICES] = {};
+    const int d = current_device();
+    if (!sms[d]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+        sms[d] = v > 0 ? v : 148;
+    }
+    return sms[d];
+}
+
+// occupancy of `kern` at (threads, smem) on the current device; the first use
+// on a device also opts the kernel into `smem` bytes of dynamic shared memory
+struct KernelDevCache {
+    int occ[MAX_DEVICES] = {};
+};
+
+template <typename K>
+inline int kernel_occupancy(K kern, int threads, size_t smem, KernelDevCache& c) {
+    const int d = current_device();
+    if (!c.occ[d]) {
+        if (smem) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
+        c.occ[d] = o > 0 ? o : 1;
+    }
+    return c.occ[d];
+}
+#endif
+
 constexpr int KEYS = QDOT_KEYS;
 constexpr int KOFF = QDOT_KEY_OFFSET;
 
@@ -110,6 +153,14 @@ __device__ __forceinline__ unsigned long long* ws_stamps(const int64_t* A) {
     return reinterpret_cast<unsigned long long*>(
         reinterpret_cast<char*>(const_cast<int64_t*>(A)) - OFF_A + OFF_LOCAL + LIST_SLOTS * 4);
 }
+// cp.async.bulk.prefetch.L2 needs a 16-byte aligned address (and size); a
+// view of a vector may be only 8-byte aligned, so prefetch from the 16-byte
+// granule holding p (inside the same allocation).  A hint: the 8 bytes this
+// drops at the end of the range do not matter.
+__device__ __forceinline__ const void* bulk_aligned(const void* p) {
+    return reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(p) & ~static_cast<uintptr_t>(15));
+}
+
 // programmatic dependent launch (the kernels of one call are launched with
 // programmatic stream serialization): a kernel may start while its
 // predecessor drains, and waits here before touching the workspace

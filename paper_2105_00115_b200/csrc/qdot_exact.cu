@@ -273,8 +273,8 @@ __device__ __forceinline__ void x_stream(XShared& S, const double* __restrict__ 
         if (t != (int64_t)blockIdx.x) x_load<NORM>(ta, x, y, t, tid);
         if (PFD > 0 && tid == 0 && t + PFD * G < nfull) {
             const int64_t p0 = (t + PFD * G) * XTILE;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(x + p0), "r"(XTILE * 8) : "memory");
-            if (!NORM) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(y + p0), "r"(XTILE * 8) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(qd::bulk_aligned(x + p0)), "r"(XTILE * 8) : "memory");
+            if (!NORM) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(qd::bulk_aligned(y + p0)), "r"(XTILE * 8) : "memory");
         }
 #pragma unroll
         for (int j = 0; j < 2 * XV; ++j) {
@@ -431,26 +431,13 @@ __global__ void __launch_bounds__(32, 1) k_exact_finalize(int64_t* __restrict__ 
 
 static_assert(sizeof(qdot_exact_result) <= 16 * 8, "exact result block");
 
-int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (!sms) sms = 148;
-    }
-    return sms;
-}
+int sm_count() { return qd::device_sm_count(); }
 
 template <bool NORM, int PFD>
 cudaError_t launch_exact_t(const double* x, const double* y, int64_t n, int64_t* ws, cudaStream_t st) {
     auto kern = k_exact<NORM, PFD>;
-    static int occ = 0;
-    if (!occ) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(XShared));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, XT, sizeof(XShared));
-        if (occ < 1) occ = 1;
-    }
+    static qd::KernelDevCache cache;
+    const int occ = qd::kernel_occupancy(kern, XT, sizeof(XShared), cache);
     const int64_t ntiles = (n + XTILE - 1) / XTILE;
     int64_t grid = (int64_t)sm_count() * occ;
     if (grid > ntiles) grid = ntiles;

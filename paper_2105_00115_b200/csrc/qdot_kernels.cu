@@ -876,36 +876,15 @@ __global__ void __launch_bounds__(256) k_begin(ulonglong2* __restrict__ p, int64
         p[i] = make_ulonglong2(0ull, 0ull);
 }
 
-static int sm_count_cached() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (!sms) sms = 148;
-    }
-    return sms;
-}
-
-template <typename K>
-static int occupancy(K kern, int threads, size_t smem) {
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-    return occ > 0 ? occ : 1;
-}
+static int sm_count_cached() { return device_sm_count(); }
 
 template <bool NORM, bool VEC, int V, bool PF, int L2D, bool SMALL = false>
 static cudaError_t launch_pass1_t(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
                                   const P1Params& prm, cudaStream_t st) {
     auto kern = k_pass1<NORM, VEC, V, PF, L2D, SMALL>;
     const size_t smem = sizeof(P1Shared);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    static int occ = 0;
-    if (!occ) occ = occupancy(kern, P1_T, smem);
+    static KernelDevCache cache;
+    const int occ = kernel_occupancy(kern, P1_T, smem, cache);
     const int64_t tile = (int64_t)P1_T * 2 * V;
     int64_t ntiles = (n + tile - 1) / tile;
     int64_t grid = (int64_t)sm_count_cached() * occ;
@@ -968,11 +947,8 @@ cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, u
                          qdot_result* res, qdot_bin* bins, int64_t n_total, const qdot_config& cfg,
                          bool fuse, cudaStream_t st) {
     const size_t smem = sizeof(ScShared);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    static KernelDevCache cache;
+    kernel_occupancy(k_score, SC_T, smem, cache);   // per-device shared-memory opt-in
     return launch_pdl(k_score, 1, SC_T, smem, st, A, B, lut_bin, lut_p2, meta, res, bins, n_total, cfg, fuse ? 1 : 0);
 }
 
@@ -996,13 +972,8 @@ static cudaError_t launch_pass2_t(const double* x, const double* y, int64_t n, c
                                   const P2Fin& fin, cudaStream_t st) {
     auto kern = k_pass2<NORM, VEC>;
     const size_t smem = sizeof(P2Shared);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    static int occ = 0;
-    if (!occ) occ = occupancy(kern, P2_T, smem);
+    static KernelDevCache cache;
+    const int occ = kernel_occupancy(kern, P2_T, smem, cache);
     int64_t ntiles = (n + P2_TILE - 1) / P2_TILE;
     int64_t grid = (int64_t)sm_count_cached() * occ;
     if (grid > ntiles) grid = ntiles;
@@ -1076,8 +1047,8 @@ static cudaError_t launch_batched_t(const double* X, const double* Y, int64_t ro
                                     const BParams& prm, double* values, int64_t* counts, int32_t* info,
                                     cudaStream_t st) {
     auto kern = k_batched<NORM, VEC>;
-    static int occ = 0;
-    if (!occ) occ = occupancy(kern, B_WARPS * 32, 0);
+    static KernelDevCache cache;
+    const int occ = kernel_occupancy(kern, B_WARPS * 32, 0, cache);
     int64_t grid = (rows + B_WARPS - 1) / B_WARPS;
     int64_t cap = (int64_t)sm_count_cached() * occ;
     if (grid > cap) grid = cap;

@@ -394,10 +394,10 @@ __device__ __forceinline__ void p1_prefetch_l2(const double* x, const double* y,
 #else
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 #endif
-    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(x + e0), "r"(TILE * 8), "l"(pol)
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(bulk_aligned(x + e0)), "r"(TILE * 8), "l"(pol)
                  : "memory");
     if (!NORM)
-        asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(y + e0), "r"(TILE * 8),
+        asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(bulk_aligned(y + e0)), "r"(TILE * 8),
                      "l"(pol) : "memory");
 }
 

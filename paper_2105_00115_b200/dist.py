@@ -53,6 +53,74 @@ def reduce_regions(region_a, region_b=None, group=None) -> None:
         dist.all_reduce(region_b, op=dist.ReduceOp.SUM, group=group)
 
 
+def _p2p(tensor, peer: int, send: bool, group) -> None:
+    """send / recv of a small tensor; gloo groups move it through host memory."""
+    import torch.distributed as dist
+    if group is not None:
+        peer = dist.get_global_rank(group, peer)
+    if dist.get_backend(group) == "gloo" and tensor.is_cuda:
+        h = tensor.cpu()
+        if send:
+            dist.send(h, dst=peer, group=group)
+        else:
+            dist.recv(h, src=peer, group=group)
+            tensor.copy_(h)
+        return
+    (dist.send if send else dist.recv)(tensor, peer, group=group)
+
+
+def chain_in_rank_order(chain, run, group=None) -> None:
+    """Run `run(chain)` rank after rank: rank r receives rank r-1's chain
+    values into `chain` before its run and sends them on after it; then every
+    rank receives the last rank's values (broadcast)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if rank > 0:
+        _p2p(chain, rank - 1, False, group)
+    run(chain)
+    if rank < world - 1:
+        _p2p(chain, rank + 1, True, group)
+    last = dist.get_global_rank(group, world - 1) if group is not None else world - 1
+    if dist.get_backend(group) == "gloo" and chain.is_cuda:
+        h = chain.cpu()
+        dist.broadcast(h, src=last, group=group)
+        chain.copy_(h)
+    else:
+        dist.broadcast(chain, src=last, group=group)
+
+
+def half_chain_sharded(xd, yd, n: int, norm: bool, st, stream: int, group=None) -> None:
+    """HALF bins flagged order-sensitive over contiguous shards: every rank
+    orders its members of those bins (stage 1), then the fp32 running sums
+    run rank after rank -- rank r continues from rank r-1's chain values
+    (stage 2, a send/recv of n_bins floats) -- and every rank applies the last
+    rank's chains (stage 4).  The value equals one device's on the
+    concatenated vectors (the reference's index-order fp32 sum)."""
+    import torch
+    from .kernel import _bin_rows
+    from .scoring import PrecisionLevel
+    lib = _lib.load()
+    nb = int(st.result.n_bins)
+    rows = _bin_rows(st.bins, nb)
+    flagged = rows[(rows["precision"] == PrecisionLevel.HALF.code) & ((rows["flags"] & 1) != 0)]
+    m = min(n, int(flagged["cardinality"].sum())) if flagged.size else 0
+    nbytes = int(lib.qdot_b200_order_scratch_bytes(n, nb))
+    scratch = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=xd.device)
+    order = torch.empty(max(m, 1), dtype=torch.int64, device=xd.device)
+    chain = torch.zeros(max(nb, 1), dtype=torch.float32, device=xd.device)
+    xp = xd.data_ptr()
+    yp = xp if norm else yd.data_ptr()
+
+    def stage(k):
+        _lib.check(lib.qdot_b200_half_ordered(xp, yp, n, int(norm), st.ws_ptr, nb, order.data_ptr(), m,
+                                              chain.data_ptr(), scratch.data_ptr(), nbytes, k, stream), lib)
+    stage(1)
+    chain_in_rank_order(chain, lambda c: stage(2), group)
+    stage(4)
+    del order, scratch
+    _lib.check(lib.qdot_b200_fetch(st.ws_ptr, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, stream), lib)
+
+
 class _ShardedIndexer:
     """Bin.indices of a sharded report would need an all-gather; refuse loudly."""
 
@@ -110,6 +178,8 @@ def qdot_sharded(x_local, y_local, cfg: ToleranceConfig, strategy: Strategy = No
     dist.all_reduce(st.region_b(), op=dist.ReduceOp.SUM, group=group)
     _lib.check(lib.qdot_b200_finalize(ws, s), lib)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
+    if st.result.half_order_sensitive == 1 and st.result.status == _lib.QDOT_OK:
+        half_chain_sharded(xd, yd, n, is_norm, st, s, group)
     _raise_status(st.result)
     phase = {"select": 0, "compute": 0, "reference": 0}
     return report_from_result(st.result, st.bins, cfg, strategy, is_norm, reference, phase, _ShardedIndexer())

@@ -54,7 +54,8 @@ class QdotReport:
     params: Optional[ParameterSet] = None
     # B200 extras (not in the reference report)
     pass2_needed: bool = False
-    half_order_sensitive: bool = False
+    half_order_sensitive: bool = False   # a HALF bin's fp32 sequential sum depends on order ...
+    half_ordered: bool = False           # ... and was replayed in index order (the value is the reference's)
 
     def count(self, level: PrecisionLevel) -> int:
         return self.counts.get(level, 0)
@@ -64,34 +65,85 @@ class QdotReport:
 
 
 class _Indexer:
-    """Materialises Bin.indices / ParameterSet.zero_idx on first access with a
-    device pass (qdot_b200_bin_ids) and a stable device sort by bin id."""
+    """Materialises Bin.indices / ParameterSet.zero_idx on first access with
+    the device counting-sort scatter (qdot_b200_bin_order: members of every
+    bin in ascending index order, binning.py:46-55,88-116) and one D2H copy.
 
-    def __init__(self, xd, yd, n, norm, device):
-        self.xd, self.yd, self.n, self.norm, self.device = xd, yd, n, norm, device
+    Device inputs the caller owns are re-read at that point: an in-place
+    modification after qdot() returned is detected (tensor version counter)
+    and raises instead of slicing stale cardinalities.  Host inputs are kept
+    as host tensors (no device copy stays alive) and uploaded again."""
+
+    def __init__(self, xd, yd, n, norm, device, host=None):
+        self.n, self.norm, self.device = n, norm, device
+        if host is not None:                      # (xh, yh) host tensors
+            self.xd = self.yd = None
+            self.host = host
+            self.version = None
+        else:
+            self.xd, self.yd, self.host = xd, yd, None
+            self.version = (xd._version, yd._version)
         self.done = False
+
+    def _inputs(self):
+        import torch
+        if self.host is not None:
+            xh, yh = self.host
+            xd = xh.to(self.device)
+            return xd, (xd if self.norm else yh.to(self.device))
+        if (self.xd._version, self.yd._version) != self.version:
+            raise RuntimeError("qdot inputs were modified in place after the call; "
+                               "Bin.indices would not match the report's bins")
+        return self.xd, self.yd
 
     def materialize(self, params: ParameterSet) -> None:
         if self.done:
             return
         import torch
         lib = _lib.load()
+        xd, yd = self._inputs()
         lut = np.full(_lib.KEYS, -1, dtype=np.int32)
         for b_id, b in enumerate(params.bins):
             lut[b.first_key:b.last_key + 1] = b_id
+        nb = len(params.bins)
         lut_d = torch.from_numpy(lut).to(self.device)
-        ids = torch.empty(max(self.n, 1), dtype=torch.int32, device=self.device)
+        nbytes = int(lib.qdot_b200_order_scratch_bytes(self.n, nb))
+        scratch = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=self.device)
+        starts_d = torch.empty(nb + 2, dtype=torch.int64, device=self.device)
+        order_d = torch.empty(max(self.n, 1), dtype=torch.int64, device=self.device)
         st = stream_handle(self.device)
-        _lib.check(lib.qdot_b200_bin_ids(self.xd.data_ptr(), self.yd.data_ptr(), self.n, int(self.norm),
-                                         lut_d.data_ptr(), ids.data_ptr(), st), lib)
-        order = torch.sort(ids[:self.n], stable=True).indices.cpu().numpy().astype(np.int64)
-        pos = params.zero_count
-        params._zero_idx = order[:pos].copy()
-        for b in params.bins:
-            b.indices = order[pos:pos + b.cardinality].copy()
-            pos += b.cardinality
+        _lib.check(lib.qdot_b200_bin_order(xd.data_ptr(), yd.data_ptr(), self.n, int(self.norm), lut_d.data_ptr(),
+                                           nb, None, starts_d.data_ptr(), order_d.data_ptr(), scratch.data_ptr(),
+                                           nbytes, st), lib)
+        starts = starts_d.cpu().numpy()
+        order = order_d[:self.n].cpu().numpy()
+        params._zero_idx = order[starts[0]:starts[1]]
+        for i, b in enumerate(params.bins):
+            b.indices = order[starts[i + 1]:starts[i + 2]]
         self.done = True
-        self.xd = self.yd = None
+        self.xd = self.yd = self.host = None
+
+
+def resolve_half_order(xd, yd, n: int, norm: bool, st, stream: int) -> None:
+    """HALF bins finalize flagged order-sensitive: replay the reference's
+    sequential fp32 sum in index order on the device (emulate.py:150-151),
+    re-fold, and refresh st.result / st.bins (qdot_b200_half_ordered)."""
+    import torch
+    lib = _lib.load()
+    res = st.result
+    nb = int(res.n_bins)
+    rows = _bin_rows(st.bins, nb)
+    flagged = rows[(rows["precision"] == PrecisionLevel.HALF.code) & ((rows["flags"] & 1) != 0)]
+    m = int(flagged["cardinality"].sum()) if flagged.size else 0
+    nbytes = int(lib.qdot_b200_order_scratch_bytes(n, nb))
+    scratch = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=xd.device)
+    order = torch.empty(max(m, 1), dtype=torch.int64, device=xd.device)
+    chain = torch.empty(max(nb, 1), dtype=torch.float32, device=xd.device)
+    xp = xd.data_ptr()
+    yp = xp if norm else yd.data_ptr()
+    _lib.check(lib.qdot_b200_half_ordered(xp, yp, n, int(norm), st.ws_ptr, nb, order.data_ptr(), m,
+                                          chain.data_ptr(), scratch.data_ptr(), nbytes, 7, stream), lib)
+    _lib.check(lib.qdot_b200_fetch(st.ws_ptr, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, stream), lib)
 
 
 def run_device(xd, yd, n: int, norm: bool, cfg: ToleranceConfig, strategy, st=None, timing: bool = True,
@@ -111,6 +163,8 @@ def run_device(xd, yd, n: int, norm: bool, cfg: ToleranceConfig, strategy, st=No
         _lib.check(lib.qdot_b200_dot(xp, yp, n, int(norm), ctypes.byref(c), ws, ctypes.byref(st.result), st.bins,
                                      _lib.KEYS + 1, s), lib)
         res = st.result
+        if res.half_order_sensitive == 1 and res.status == _lib.QDOT_OK:
+            resolve_half_order(xd, yd, n, norm, st, s)
         return res, st.bins, {"select": int(res.select_ns), "compute": int(res.compute_ns), "reference": 0}
     torch_stream = None
     if timing:
@@ -127,6 +181,8 @@ def run_device(xd, yd, n: int, norm: bool, cfg: ToleranceConfig, strategy, st=No
     if torch_stream is not None:
         st.ev[2].record(torch_stream)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
+    if st.result.half_order_sensitive == 1 and st.result.status == _lib.QDOT_OK:
+        resolve_half_order(xd, yd, n, norm, st, s)
     phase = {"select": 0, "compute": 0, "reference": 0}
     if torch_stream is not None:
         phase["select"] = int(st.ev[0].elapsed_time(st.ev[1]) * 1e6)
@@ -269,7 +325,7 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
         rel_bound_e=rel_bound_e, early_terminated=params.early_terminated, n=params.n,
         epsilon=cfg.epsilon, split=cfg.split, strategy=strategy_label(params.strategy),
         phase_ns=phase, params=params, pass2_needed=bool(res.pass2_needed),
-        half_order_sensitive=bool(res.half_order_sensitive))
+        half_order_sensitive=bool(res.half_order_sensitive), half_ordered=int(res.half_order_sensitive) == 2)
 
 
 # host inputs at least this long are streamed to the device in chunks that
@@ -345,6 +401,8 @@ def _run_host_pipelined(xh, yh, norm: bool, cfg: ToleranceConfig, strategy):
     _lib.check(lib.qdot_b200_pass2_finalize(xd.data_ptr(), yd.data_ptr(), n, int(norm), ws, s), lib)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, _lib.KEYS + 1, s), lib)
     res = st.result
+    if res.half_order_sensitive == 1 and res.status == _lib.QDOT_OK:
+        resolve_half_order(xd, yd, n, norm, st, s)
     phase = {"select": int(res.select_ns), "compute": int(res.compute_ns), "reference": 0}
     return res, st.bins, phase, xd, yd
 
@@ -370,7 +428,8 @@ def qdot(x, y, cfg: ToleranceConfig, strategy: Strategy = None, reference=None) 
             n = int(xh.shape[0])
             res, cbins, phase, xd, yd = _run_host_pipelined(xh, yh, is_norm, cfg, strategy)
             _raise_status(res)
-            indexer = _Indexer(xd, yd, n, is_norm, xd.device)
+            indexer = _Indexer(None, None, n, is_norm, xd.device, host=(xh, yh))
+            del xd, yd
             return report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer)
     is_norm, xd, yd = _prepare(x, y)
     n = int(xd.shape[0])

@@ -50,6 +50,22 @@ def checksum(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()[:16]
 
 
+def members_sha(ps) -> str:
+    """Digest of the member order: zero_idx then every bin's indices, int64."""
+    h = hashlib.sha256(np.ascontiguousarray(ps.zero_idx, dtype=np.int64).tobytes())
+    for b in ps.bins:
+        h.update(b"|")
+        h.update(np.ascontiguousarray(b.indices, dtype=np.int64).tobytes())
+    return h.hexdigest()[:16]
+
+
+def half_seq_inputs(n: int = 1 << 18, seed: int = 21):
+    """Positive products whose HALF bins' fp32 running sums leave the exact
+    range of fp32 (the reference's sequential sum then rounds, order-sensitively)."""
+    rng = np.random.default_rng(seed)
+    return np.abs(rng.standard_normal(n)), np.abs(rng.standard_normal(n))
+
+
 def run_case(name, x, y, eps, split, strategy, input_mu=52, norm=False, store=True, key=None):
     cfg = ToleranceConfig(epsilon=eps, split=SplitMode.PER_BIN if split == "per-bin" else SplitMode.NONE,
                           input_mu=input_mu)
@@ -80,6 +96,7 @@ def run_case(name, x, y, eps, split, strategy, input_mu=52, norm=False, store=Tr
         "bins": [[int(b.lower), int(b.upper), int(b.cardinality), int(b.score),
                   PREC[b.precision.label], float(bin_dot(xx, yy, b)).hex()]
                  for b in ps.bins],
+        "members_sha": members_sha(ps),
     })
     try:
         ref = reference_dot(xx, yy)
@@ -189,6 +206,13 @@ def main():
     add("C1_ranged4", x, y, 1e-8, "none", "ranged:4", store=False)
     add("C1_split5", x, y, 1e-8, "none", "split:5", store=False)
     add("C1_loose", x, y, 1e-3, "per-bin", "exact", store=False)
+    # HALF bins with 2^13..2^17 positive members: the fp32 running sums round
+    # (order-sensitive), so the device must replay them in index order
+    x, y = half_seq_inputs()
+    for st in ["exact", "ranged:4", "split:3"]:
+        for sp in ["none", "per-bin"]:
+            add(f"half_seq_{st}_{sp}", x, y, 2.0**10, sp, st, store=False)
+    add("half_seq_norm", x, x, 2.0**8, "none", "exact", norm=True, store=False)
     x, y = gen_illcond(1 << 20, seed=0)
     add("C3_2e20", x, y, 1e-12, "none", "exact", store=False)
     add("C3_2e20_perbin", x, y, 1e-12, "per-bin", "exact", store=False)

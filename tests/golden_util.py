@@ -36,6 +36,9 @@ def _regen(name):
         return gen_normal(1 << 20, seed=0)
     if name.startswith("C3"):
         return gen_illcond(1 << 20, seed=0)
+    if name.startswith("half_seq"):
+        rng = np.random.default_rng(21)
+        return np.abs(rng.standard_normal(1 << 18)), np.abs(rng.standard_normal(1 << 18))
     raise KeyError(name)
 
 
@@ -65,3 +68,13 @@ def select(pred=None, max_n=None):
         if pred is None or pred(c):
             out.append(c)
     return out
+
+
+def members_sha(zero_idx, bin_indices) -> str:
+    """Digest of the member order (make_golden.members_sha): zero_idx, then
+    each bin's indices, as int64."""
+    h = hashlib.sha256(np.ascontiguousarray(zero_idx, dtype=np.int64).tobytes())
+    for ind in bin_indices:
+        h.update(b"|")
+        h.update(np.ascontiguousarray(ind, dtype=np.int64).tobytes())
+    return h.hexdigest()[:16]

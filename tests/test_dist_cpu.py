@@ -20,7 +20,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2105_00115_b200 import _lib
-from paper_2105_00115_b200.dist import reduce_regions, shard_bounds
+from paper_2105_00115_b200.dist import chain_in_rank_order, reduce_regions, shard_bounds
 
 KEYS, KOFF = _lib.KEYS, _lib.KEY_OFFSET
 
@@ -99,6 +99,51 @@ def test_gloo_region_exchange_is_exact(world, n):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res == (True, True, True)
+
+
+def _chain_worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        vals = np.abs(rng.standard_normal((3, n))).astype(np.float16).astype(np.float32)   # 3 "bins"
+        lo, hi = shard_bounds(n, rank, world)
+        chain = torch.zeros(3, dtype=torch.float32)
+
+        def run(c):                                  # this rank's part of each fp32 running sum
+            for b in range(3):
+                s = np.float32(c[b].item())
+                for v in vals[b, lo:hi]:
+                    s = np.float32(s + v)
+                c[b] = float(s)
+        chain_in_rank_order(chain, run)
+        want = []
+        for b in range(3):                           # emulate.py:105-108 over the whole vector
+            s = np.float32(0.0)
+            for v in vals[b]:
+                s = np.float32(s + v)
+            want.append(float(s))
+        q.put((rank, chain.tolist() == want))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_half_chain_runs_in_rank_order(world):
+    """The HALF order-sensitive fallback over shards (dist.half_chain_sharded):
+    fp32 running sums continued rank after rank equal the single sequential sum."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, world, port, 30011, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(res.values()) and len(res) == world
 
 
 def test_shard_bounds_partition():

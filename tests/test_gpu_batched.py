@@ -28,11 +28,8 @@ def check_rows(X, Y, rep, eps, split="none", strategy="exact"):
         if o.n_bins:
             assert (rep.e_min[r], rep.e_max[r]) == (o.e_min, o.e_max), r
         assert bool(rep.early_terminated[r]) == o.early_terminated
-        if rep.half_order_sensitive[r]:
-            assert abs(rep.values[r] - o.value) <= o.abs_cap, r
-        else:
-            assert rep.values[r] == o.value or (math.isnan(o.value) and math.isnan(rep.values[r])), \
-                (r, rep.values[r], o.value)
+        assert rep.values[r] == o.value or (math.isnan(o.value) and math.isnan(rep.values[r])), \
+            (r, rep.values[r], o.value)
 
 
 def test_c4_golden_rows():
@@ -58,8 +55,7 @@ def test_golden_mixed_rows():
         rep = Q.qdot_batched(x[None, :], y[None, :], cfg)
         assert rep.n_bins[0] == c["n_bins"], c["name"]
         assert {LABELS[k]: int(rep.counts[0, k]) for k in range(4)} == c["counts"], c["name"]
-        if not rep.half_order_sensitive[0]:
-            assert rep.values[0] == G.hexf(c["value"]), c["name"]
+        assert rep.values[0] == G.hexf(c["value"]), c["name"]
 
 
 @pytest.mark.parametrize("eps,split", [(1e-6, "none"), (1e-3, "per-bin"), (1e-10, "none"), (1e-1, "none")])

@@ -2,11 +2,14 @@
 golden outputs and the CPU oracle.
 
 Bar (DESIGN.md "Parity"): bins, scores, precisions, counts, bounds and
-error behaviour bit-exact; per-bin values and the final value bit-exact
-wherever the reference's own accumulation is exact (always for SINGLE /
-DOUBLE in practice; HALF bins flagged order-sensitive fall back to the
-per-bin budget M * 2^(u+1) * eps); every value within abs_cap of the
-reference value and of the exact dot.
+error behaviour bit-exact; per-bin values and the final value bit-exact.
+HALF bins whose fp32 sequential sum is order-sensitive are replayed in index
+order on the device (qdot_b200_half_ordered), so they are held to the same
+bar.  The one admitted difference: a DOUBLE bin where the reference's
+Neumaier sum is itself not the correctly rounded sum of its products (the
+device rounds the exact sum once) -- checked explicitly with math.fsum over
+the bin's members, and it never occurs in the golden set.  Every value lies
+within abs_cap of the exact dot.
 """
 
 import math
@@ -44,6 +47,29 @@ def same(a, b):
     return a == b or (math.isnan(a) and math.isnan(b))
 
 
+NEUMAIER_NOT_CR = []   # (bin, oracle value, fsum) of DOUBLE bins where the reference is not correctly rounded
+
+
+def assert_bins_exact(x, y, rep, r):
+    """Per-bin values and the value equal the oracle's bit for bit, except a
+    DOUBLE bin whose reference (Neumaier, index order) value is not the
+    correctly rounded sum of its products: there the device value must be the
+    correctly rounded one (math.fsum) and the final value within abs_cap."""
+    exact = True
+    for b, w in zip(rep.params.bins, r.bins):
+        if same(b.value, w.value):
+            continue
+        assert b.precision is P.DOUBLE, (b, b.value, w.value)
+        cr = math.fsum((x[w.indices] * y[w.indices]).tolist())
+        assert b.value == cr and w.value != cr, (b, b.value, w.value, cr)
+        NEUMAIER_NOT_CR.append((b.upper, w.value, cr))
+        exact = False
+    if exact:
+        assert same(rep.value, r.value), (rep.value, r.value)
+    else:
+        assert abs(rep.value - r.value) <= rep.abs_cap
+
+
 def check_against_golden(case, rep):
     bins = rep.params.bins
     got = [[b.lower, b.upper, b.cardinality, b.score, b.precision.code] for b in bins]
@@ -59,21 +85,12 @@ def check_against_golden(case, rep):
     assert rep.rel_bound == G.hexf(case["rel_bound"])
     assert rep.rel_guarantee == G.hexf(case["rel_guarantee"])
     assert rep.abs_cap == G.hexf(case["abs_cap"])
-    # per-bin values
-    exact_bins = True
+    # per-bin values: bit-exact, every precision (the reference's DOUBLE
+    # Neumaier sums are correctly rounded on every golden input)
     for b, w in zip(bins, case["bins"]):
-        want = G.hexf(w[5])
-        if same(b.value, want):
-            continue
-        exact_bins = False
-        assert b.flags & 1 or b.precision is P.DOUBLE, (case["name"], b, b.value, want)
-        budget = b.cardinality * math.ldexp(b.precision.eps, b.upper + 1)
-        assert abs(b.value - want) <= budget, (case["name"], b)
+        assert same(b.value, G.hexf(w[5])), (case["name"], b, b.value, w[5])
     want = G.hexf(case["value"])
-    if exact_bins:
-        assert same(rep.value, want), (case["name"], rep.value.hex(), case["value"])
-    else:
-        assert abs(rep.value - want) <= rep.abs_cap
+    assert same(rep.value, want), (case["name"], rep.value.hex(), case["value"])
     if case.get("exact") is not None and math.isfinite(rep.value):
         assert abs(rep.value - G.hexf(case["exact"])) <= rep.abs_cap + 1e-300
 
@@ -103,6 +120,9 @@ def test_golden_case(case, pass1_mode):
     rep = Q.qdot(x, yy, cfg, strategy=strat(case["strategy"]))
     check_against_golden(case, rep)
     assert rep.rel_hypothesis == case["rel_hypothesis"]
+    if pass1_mode == 0:   # Bin.indices / zero_idx (device counting-sort scatter) against the reference's order
+        ps = rep.params
+        assert G.members_sha(ps.zero_idx, [b.indices for b in ps.bins]) == case["members_sha"], case["name"]
 
 
 @pytest.mark.parametrize("seed", range(12))
@@ -117,15 +137,11 @@ def test_random_against_oracle(seed, strategy, pass1_mode):
         x[rng.integers(0, n, max(1, n // 50))] = 0.0
     eps = float(np.ldexp(1.0, -int(rng.integers(0, 55))))
     split = "per-bin" if seed % 2 else "none"
-    r = O.qdot(x, y, eps, split, 52, strategy)
+    r = O.qdot(x, y, eps, split, 52, strategy, members=True)
     rep = Q.qdot(x, y, Q.ToleranceConfig(eps, Q.SplitMode(split)), strategy=strat(strategy))
     assert [[b.lower, b.upper, b.cardinality, b.score, b.precision.code] for b in rep.params.bins] == \
         [[b.lower, b.upper, b.cardinality, b.score, b.precision] for b in r.bins]
-    for b, w in zip(rep.params.bins, r.bins):
-        if not same(b.value, w.value):
-            assert b.flags & 1 or b.precision is P.DOUBLE
-            assert abs(b.value - w.value) <= b.cardinality * math.ldexp(b.precision.eps, b.upper + 1)
-    assert abs(rep.value - r.value) <= rep.abs_cap
+    assert_bins_exact(x, y, rep, r)
     ex, _, _ = O.exact_dot(x, y)
     assert abs(rep.value - ex) <= rep.abs_cap
 
@@ -158,6 +174,21 @@ def test_torch_inputs_and_misaligned_views():
     assert rep.value == want
     rep2 = Q.qdot(xt[1:].clone(), yt[1:].clone(), Q.ToleranceConfig(1e-9))
     assert rep2.value == want
+
+
+@pytest.mark.parametrize("n", [(1 << 21) + 7, (1 << 23) + 1])
+def test_misaligned_views_of_long_vectors(n):
+    """8-byte aligned views long enough for the streaming pass-1 variant (its
+    TMA L2 prefetch needs 16-byte addresses): same value as aligned copies,
+    and the device exact dot agrees too."""
+    x, y = O.gen_normal(n + 1, seed=12)
+    xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    for strategy in ("exact", "ranged:3"):
+        a = Q.qdot(xt[1:], yt[1:], Q.ToleranceConfig(1e-9), strategy=strat(strategy))
+        b = Q.qdot(xt[1:].clone(), yt[1:].clone(), Q.ToleranceConfig(1e-9), strategy=strat(strategy))
+        assert a.value == b.value and a.counts == b.counts
+    assert a.value == O.qdot(x[1:], y[1:], 1e-9, "none", 52, "ranged:3").value
+    assert Q.reference_dot(xt[1:], yt[1:]).value == Q.reference_dot(xt[1:].clone(), yt[1:].clone()).value
 
 
 def test_lazy_indices_match_oracle():
@@ -419,8 +450,13 @@ def test_pass2_finalize_sequences_agree(strategy, eps, n):
     assert outs[0] == outs[1] == outs[2]
     if n:
         ref = O.qdot(x.cpu().numpy(), y.cpu().numpy(), eps, "none", 52, strategy)
-        if outs[0][5]:   # a HALF bin the reference sums order-sensitively in fp32: its budget applies
-            assert abs(outs[0][0] - ref.value) <= ref.abs_cap
+        if outs[0][5]:   # a HALF bin the reference sums order-sensitively in fp32: replay it in index order
+            from paper_2105_00115_b200.kernel import resolve_half_order
+            st.result = res
+            ctypes.memmove(st.bins, bins, ctypes.sizeof(bins))
+            resolve_half_order(x, y, n, False, st, s)
+            assert st.result.half_order_sensitive == 2
+            assert st.result.value == ref.value
         else:
             assert outs[0][0] == ref.value
 
@@ -432,8 +468,7 @@ def test_inputs_written_just_before_the_call_are_seen(n):
     rewrites x and y on the same stream with no host sync in between: each
     call must see the new data (eager launches and the cached graph path)."""
     def agree(rep, ref):
-        # a HALF bin the reference sums order-sensitively in fp32: its budget applies
-        return abs(rep.value - ref.value) <= ref.abs_cap if rep.half_order_sensitive else rep.value == ref.value
+        return rep.value == ref.value
 
     rng = np.random.default_rng(n)
     xs = [rng.standard_normal(n) * np.exp2(rng.integers(-20, 20, n)) for _ in range(4)]

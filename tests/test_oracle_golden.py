@@ -26,7 +26,9 @@ def test_oracle_matches_reference(case):
         with pytest.raises(exc):
             O.qdot(x, y, G.hexf(case["epsilon"]), case["split"], case["input_mu"], case["strategy"])
         return
-    r = O.qdot(x, y, G.hexf(case["epsilon"]), case["split"], case["input_mu"], case["strategy"])
+    r = O.qdot(x, y, G.hexf(case["epsilon"]), case["split"], case["input_mu"], case["strategy"], members=True)
+    zero_idx = np.flatnonzero((x == 0) | (y == 0))
+    assert G.members_sha(zero_idx, [b.indices for b in r.bins]) == case["members_sha"]
     got_bins = [[b.lower, b.upper, b.cardinality, b.score, b.precision] for b in r.bins]
     want_bins = [b[:5] for b in case["bins"]]
     assert got_bins == want_bins
