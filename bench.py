@@ -5,11 +5,16 @@
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 Workload (BASELINE.json configs[1]): qdot of two
-standard-normal fp64 vectors of n = 2^28 per GPU (default_rng(0), x then y),
-epsilon = 1e-8, SplitMode.NONE, ExactBinning.  At N > 1 every rank holds its
-own 2^28-element shard of one N*2^28-element dot product (C5 at N = 8) and
-the ranks exchange the exponent histogram and the exact per-key partial sums
-over NCCL (weak scaling).  A "step" is one full qdot: begin + pass1 +
+standard-normal fp64 vectors of n = 2^28 per GPU, epsilon = 1e-8,
+SplitMode.NONE, ExactBinning.  N = 1: the C2 golden input (numpy
+default_rng(0), x then y).  N > 1 (weak scaling): rank r holds elements
+[r 2^28, (r+1) 2^28) of one N*2^28-element vector pair drawn by the device
+generator (csrc/qdot_gen.cu, standard-normal law, index-keyed, so the shards
+of every N are slices of the same global vectors; N = 8 is C5, n = 2^31).
+--n-total M: strong scaling over one fixed M-element pair (C5: M = 2^31)
+sharded with dist.shard_bounds; every N prints the same value_check and
+bins_hash.  The ranks exchange the exponent histogram and the exact per-key
+partial sums over NCCL.  A "step" is one full qdot: begin + pass1 +
 allreduce(A) + score + pass2 + allreduce(B) + finalize.
 
 `value` = elements/s with inputs resident in HBM (CUDA events, max over
@@ -20,9 +25,15 @@ overlapping pass 1 on chunk k, so e2e runs at the PCIe H2D rate).
 Inputs (4 GiB per GPU) are far larger than the 126 MB L2, so no L2 flush is
 needed between steps.
 
---impl reference times the CPU oracle port (oracle/qdot_oracle.c, the C
-restatement of the reference path; the reference itself is Python and is
-not installable on the GPU box) on a bounded sample with all host threads.
+--impl reference times the reference's own CPU implementation: the
+unmodified qdot 0.1.0 package installed in baseline/_ref (pure Python +
+NumPy + numba, single-threaded: cores = 1) on a bounded sample of the C2
+workload; the C oracle port (oracle/qdot_oracle.c) on all host threads is
+reported beside it, and stands in only when baseline/_ref is absent.
+
+Besides the headline (a burst: the driver's K steps), a sustained block
+re-times the step back to back for >= 1.5 s (clocks settle under the power
+cap), and e2e_numpy repeats e2e with pageable numpy inputs.
 """
 
 from __future__ import annotations
@@ -54,7 +65,14 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--elements", "--n", dest="n", type=int, default=N_PER_GPU, help="elements per GPU")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24, help="elements per step of the oracle port")
+    ap.add_argument("--ref-sample", type=int, default=1 << 24, help="elements per step of the reference")
+    ap.add_argument("--n-total", type=int, default=None,
+                    help="strong scaling: one fixed vector pair of this many elements over all ranks (C5: 2^31)")
+    ap.add_argument("--data", default="auto", choices=["auto", "numpy", "device"],
+                    help="auto: numpy C2 golden input at N=1, the device generator otherwise")
+    ap.add_argument("--sustained-ms", type=float, default=1500.0,
+                    help="re-time the step back to back for this long (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--norm", action="store_true", help="norm mode x.x (8 B/elem)")
     ap.add_argument("--no-secondary", action="store_true", help="skip the read probe and the C4 batched line")
@@ -150,7 +168,51 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
-def cpu_baseline(n_sample: int, steps: int = 1):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_module():
+    """The unmodified reference package from baseline/_ref, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "qdot")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import qdot as R
+        if not os.path.abspath(R.__file__).startswith(REF_DIR):
+            return None
+        return R
+    except Exception:
+        return None
+
+
+def time_reference(n_sample: int, steps: int, warm: int):
+    """The reference's own qdot (kernel.py:179-240) on a C2-law sample, best of
+    `steps` after `warm` untimed calls (and a small numba JIT warm-up).  It is
+    single-threaded by construction: cores = 1."""
+    R = _reference_module()
+    if R is None:
+        return None
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(n_sample)
+    y = rng.standard_normal(n_sample)
+    cfg = R.ToleranceConfig(EPS)
+    R.qdot(x[:4096], y[:4096], cfg)                         # numba JIT
+    for _ in range(warm):
+        R.qdot(x, y, cfg)
+    times = []
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        R.qdot(x, y, cfg)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": n_sample / best, "unit": "elements/s", "cores": 1, "kind": "reference",
+            "sample": f"reference qdot 0.1.0 (baseline/_ref, unmodified) on n={n_sample} standard-normal "
+                      f"x, y (default_rng(0)), eps=1e-8, exact; best of {len(times)} after {warm} warm-up",
+            "ms_per_call": best * 1e3, "host_cores_available": os.cpu_count()}
+
+
+def time_port(n_sample: int, steps: int = 2):
     """Oracle port (C restatement of the reference path), all host threads."""
     from oracle import oracle as O
     threads = os.cpu_count() or 1
@@ -166,6 +228,17 @@ def cpu_baseline(n_sample: int, steps: int = 1):
     return {"value": n_sample / best, "unit": "elements/s", "cores": threads, "kind": "port",
             "sample": f"qdot n={n_sample} standard-normal eps=1e-8 exact, oracle/qdot_oracle.c, "
                       f"best of {len(times)}"}
+
+
+def cpu_baseline(n_sample: int, ref_sample: int):
+    """The reference itself on 1 core (kind "reference") with the port beside
+    it; the port alone when baseline/_ref is missing."""
+    port = time_port(n_sample)
+    ref = time_reference(ref_sample, 2, 1)
+    if ref is None:
+        return port
+    ref["port"] = port
+    return ref
 
 
 def measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, norm, Q, config_struct):
@@ -301,32 +374,38 @@ def measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, norm, Q, config_
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    steps = max(1, args.steps if args.steps <= 5 else 3)
-    warm = min(args.warmup, 1)
-    from oracle import oracle as O
-    threads = os.cpu_count() or 1
-    O.set_threads(threads)
-    n_s = args.cpu_sample
-    x, y = O.gen_normal(n_s, seed=0)
-    for _ in range(warm):
-        O.qdot(x, y, EPS)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        O.qdot(x, y, EPS)
-    dt = (time.perf_counter() - t0) / steps
-    val = n_s / dt
+    steps = max(1, min(args.steps, 3))
+    warm = min(max(args.warmup, 0), 1)
+    ref = time_reference(args.ref_sample, steps, warm)
+    port = time_port(args.cpu_sample, steps)
+    base = ref if ref is not None else port
+    if ref is not None:
+        ref["port"] = port
+    val = base["value"]
+    n_s = args.ref_sample if ref is not None else args.cpu_sample
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "elements/s", "n_gpus": args.gpus,
-        "steps": steps, "warmup": warm, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "steps": steps, "warmup": warm, "ms_per_step": n_s / val * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 qdot fp64 standard-normal eps=1e-8 exact (bounded CPU sample)",
-                   "n_sample": n_s, "threads": threads},
-        "cpu_baseline": {"value": val, "unit": "elements/s", "cores": threads, "kind": "port",
-                         "sample": f"n={n_s} per step (of the 2^28 workload)"},
+        "config": {"workload": "C2 qdot fp64 standard-normal eps=1e-8 exact (bounded CPU sample of the "
+                               "2^28 workload)", "n_sample": n_s,
+                   "implementation": ("reference qdot 0.1.0 from baseline/_ref, single-threaded"
+                                      if ref is not None else "oracle/qdot_oracle.c port, all host threads")},
+        "cpu_baseline": dict(base, value=val),
         "e2e": {"value": val, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
+
+
+def bins_hash(st, nb: int) -> str:
+    """Digest of the bin table (lower, upper, M, score, precision)."""
+    import hashlib
+    h = hashlib.sha256()
+    for i in range(nb):
+        b = st.bins[i]
+        h.update(np.array([b.lower, b.upper, b.cardinality, b.score, b.precision], dtype=np.int64).tobytes())
+    return h.hexdigest()[:16]
 
 
 def main():
@@ -356,13 +435,31 @@ def main():
     from paper_2105_00115_b200.dist import reduce_regions
     lib = _lib.load()
 
-    n = args.n
-    # synthetic inputs: rank r draws its shard with default_rng(r) (rank 0 == the C2 golden input)
-    rng = np.random.default_rng(rank)
-    xh = rng.standard_normal(n)
-    yh = xh if args.norm else rng.standard_normal(n)
-    xd = torch.from_numpy(xh).to(dev)
-    yd = xd if args.norm else torch.from_numpy(yh).to(dev)
+    from paper_2105_00115_b200.dist import shard_bounds
+    from paper_2105_00115_b200.generate import device_vectors
+    strong = args.n_total is not None
+    if strong:
+        n_total = int(args.n_total)
+        lo, hi = shard_bounds(n_total, rank, world)
+    else:
+        n_total = args.n * world
+        lo, hi = rank * args.n, (rank + 1) * args.n
+    n = hi - lo
+    use_numpy = args.data == "numpy" or (args.data == "auto" and world == 1 and not strong)
+    if use_numpy:
+        # the C2 golden input: default_rng(0), x then y (rank r of a numpy run: default_rng(r))
+        rng = np.random.default_rng(rank)
+        xh = rng.standard_normal(n)
+        yh = xh if args.norm else rng.standard_normal(n)
+        xd = torch.from_numpy(xh).to(dev)
+        yd = xd if args.norm else torch.from_numpy(yh).to(dev)
+        data_desc = "numpy default_rng(rank) standard normal, x then y (rank 0 = the C2 golden input)"
+    else:
+        # elements [lo, hi) of one global pair from the index-keyed device generator
+        xd, yd = device_vectors("normal", n, seed=0, offset=lo, norm=args.norm, device=dev)
+        xh = yh = None
+        data_desc = (f"device generator (csrc/qdot_gen.cu) standard-normal law, seed 0, elements [{lo}, {hi}) "
+                     f"of one {n_total}-element pair")
     cfg = Q.ToleranceConfig(EPS)
     c = config_struct(cfg, Q.ExactBinning())
     st = thread_state(dev)
@@ -371,7 +468,6 @@ def main():
     ws = st.ws_ptr
     norm = int(args.norm)
     xp, yp = xd.data_ptr(), yd.data_ptr()
-    n_total = n * world
     ra, rb = st.region_a(), st.region_b()
     ev_p1 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
              for _ in range(args.steps)]
@@ -397,21 +493,31 @@ def main():
             reduce_regions(rb)                       # NCCL SUM of region B (exact partials)
             _lib.check(lib.qdot_b200_finalize(ws, s), lib)
 
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(*vals):
+        if world == 1:
+            return vals
+        tt = torch.tensor(list(vals), device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        return tuple(float(v) for v in tt)
+
     for _ in range(max(3, args.warmup)):
         step()
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, 4196, s), lib)
     value_check = st.result.value
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+    digest = bins_hash(st, int(st.result.n_bins))
+    n_bins = int(st.result.n_bins)
+    barrier()
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+    barrier()
     clk.mark_start()
     t0.record(stream)
     for i in range(args.steps):
@@ -419,15 +525,11 @@ def main():
     t1.record(stream)
     torch.cuda.synchronize()
     clk.mark_stop()
-    if world > 1:
-        torch.distributed.barrier()
+    barrier()
     clocks = clk.stop()
     ms = t0.elapsed_time(t1) / args.steps
     p1_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_p1)
-    if world > 1:
-        tt = torch.tensor([ms, p1_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms, p1_ms = float(tt[0]), float(tt[1])
+    ms, p1_ms = max_over_ranks(ms, p1_ms)
     value = n_total / (ms * 1e-3)
     _lib.check(lib.qdot_b200_fetch(ws, ctypes.byref(st.result), st.bins, 4196, s), lib)
     assert st.result.value == value_check, "non-deterministic result"
@@ -435,39 +537,71 @@ def main():
     pass1_modes = {"full_ctas": int(a_host[_lib.KEYS + 2]), "lean_ctas": int(a_host[_lib.KEYS + 3]),
                    "pass2_needed": bool(st.result.pass2_needed)}
 
+    # ---- sustained: the same step back to back for >= sustained_ms (the
+    # headline K steps are a burst; clocks drop under the power cap later)
+    sustained = None
+    if args.sustained_ms > 0 and ms * args.steps < args.sustained_ms:
+        ks = max(args.steps, int(args.sustained_ms / ms) + 1)
+        clk2 = ClockSampler(local)
+        clk2.start()
+        time.sleep(0.2)
+        barrier()
+        clk2.mark_start()
+        t0.record(stream)
+        for _ in range(ks):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        clk2.mark_stop()
+        barrier()
+        (ms_s,) = max_over_ranks(t0.elapsed_time(t1) / ks)
+        sustained = {"steps": ks, "ms_per_step": ms_s, "value": n_total / (ms_s * 1e-3),
+                     "hbm_gbs_step": n * (8 if args.norm else 16) / (ms_s * 1e-3) / 1e9, "clocks": clk2.stop()}
+
     # ---- e2e: public API from pinned host memory, H2D + D2H inside the timed region
     e2e = None
+    e2e_numpy = None
     if args.e2e_steps > 0:
         # public API from pinned host memory: qdot() at N=1, dist.qdot_sharded()
         # (each rank copies its own shard) at N>1; max over ranks
         from paper_2105_00115_b200.dist import qdot_sharded
-        xpin = torch.from_numpy(xh).pin_memory()
-        ypin = xpin if args.norm else torch.from_numpy(yh).pin_memory()
+        if xh is None:
+            xpin = xd.cpu().pin_memory()
+            ypin = xpin if args.norm else yd.cpu().pin_memory()
+        else:
+            xpin = torch.from_numpy(xh).pin_memory()
+            ypin = xpin if args.norm else torch.from_numpy(yh).pin_memory()
 
-        def api():
+        def api(a, b):
             if world == 1:
-                return Q.qdot(xpin, ypin, cfg)
-            return qdot_sharded(xpin, ypin, cfg, n_total=n_total)
+                return Q.qdot(a, b, cfg)
+            return qdot_sharded(a, b, cfg, n_total=n_total)
 
-        rep = api()  # warm (two calls: pinned staging, allocator, graph caches)
-        rep = api()
-        assert rep.value == value_check
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        te = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            rep = api()
-        torch.cuda.synchronize()
-        dte = (time.perf_counter() - te) / args.e2e_steps
-        if world > 1:
-            tt = torch.tensor([dte], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            dte = float(tt[0])
+        def timed(a, b):
+            rep = api(a, b)  # warm (two calls: pinned staging, allocator, graph caches)
+            rep = api(a, b)
+            assert rep.value == value_check
+            barrier()
+            te = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                rep = api(a, b)
+            torch.cuda.synchronize()
+            (dte,) = max_over_ranks((time.perf_counter() - te) / args.e2e_steps)
+            return dte
+
+        dte = timed(xpin, ypin)
         h2d = n * 8 * (1 if args.norm else 2)
         e2e = {"value": n_total / dte, "unit": "elements/s", "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": (256 + 56 * 64) * world, "ms_per_step": dte * 1e3,
-               "api": "qdot()" if world == 1 else "dist.qdot_sharded()"}
+               "api": ("qdot()" if world == 1 else "dist.qdot_sharded()") + " from pinned host tensors"}
+        if world == 1:
+            # the reference's callers pass numpy arrays (pageable memory)
+            xnp = xpin.numpy().copy()
+            ynp = xnp if args.norm else ypin.numpy().copy()
+            dtn = timed(xnp, ynp)
+            e2e_numpy = {"value": n_total / dtn, "unit": "elements/s", "ms_per_step": dtn * 1e3,
+                         "h2d_bytes_per_step": h2d, "api": "qdot() from numpy (pageable) arrays"}
+            del xnp, ynp
         del xpin, ypin
 
     peak, peak_kind = measured_peak()
@@ -489,25 +623,31 @@ def main():
         roofline["frac_of_read_probe"] = achieved / secondary["read_probe"]["GBps"]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.cpu_sample)
+        cpu = cpu_baseline(args.cpu_sample, args.ref_sample)
     if rank == 0:
+        wl = ("C5 strong scaling: one fixed fp64 standard-normal pair" if strong else
+              "C2 qdot n=2^28 fp64 standard-normal per GPU")
         line = {
             "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": ("C2 qdot n=2^28 fp64 standard-normal per GPU, eps=1e-8, split=none, exact"
-                                    + (" (norm mode x.x)" if args.norm else "")),
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic: " + data_desc,
+            "config": {"workload": wl + ", eps=1e-8, split=none, exact" + (" (norm mode x.x)" if args.norm else ""),
                        "n_per_gpu": n, "n_total": n_total, "epsilon": EPS, "strategy": "exact",
                        "parallelism": f"dp{world} contiguous shards + NCCL allreduce(hist, partials)",
-                       "l2": "inputs 4 GiB/GPU >> 126 MB L2 (no flush needed)",
-                       "hbm_gbs_step": n * bytes_per_elem * world / (ms * 1e-3) / 1e9 / world},
+                       "l2": "inputs >= 4 GiB/GPU >> 126 MB L2 (no flush needed)",
+                       "hbm_gbs_step": n * bytes_per_elem / (ms * 1e-3) / 1e9},
             "value_check": value_check,
+            "bins_hash": digest,
+            "n_bins": n_bins,
             "pass1_modes": pass1_modes,
             "clocks": clocks,
             "gpu_launches": (4 if world == 1 else 5) * args.steps,   # begin, pass1, score, pass2 (+ finalize at N > 1)
             "roofline": roofline,
+            "sustained": sustained,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_numpy": e2e_numpy,
             "secondary": secondary,
         }
         print(json.dumps(line), flush=True)

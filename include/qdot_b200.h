@@ -167,6 +167,17 @@ int qdot_b200_fetch(const void* ws, qdot_result* out, qdot_bin* bins, int32_t ma
 /* device-resident x, y: begin + pass1 + score + pass2 + finalize + fetch */
 int qdot_b200_dot(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
                   void* ws, qdot_result* out, qdot_bin* bins, int32_t max_bins, void* stream);
+/* pass 1 over HOST vectors (pageable or pinned): copies them into the caller's
+ * device buffers dx, dy (n elements each) chunk by chunk while pass 1 consumes
+ * each landed chunk on `stream`.  Pageable memory goes through the library's
+ * pinned staging ring, filled by a pool of host threads (parallel memcpy)
+ * while the DMA engine drains the previous buffer.  Returns when the host
+ * memory has been read (pageable) / all copies are enqueued (pinned).
+ * Replaces the np.ascontiguousarray hand-off of kernel.py:195-196 + pass 1. */
+int qdot_b200_pass1_host(const double* hx, const double* hy, int64_t n, int norm, const qdot_config* cfg,
+                         int64_t n_total, void* ws, double* dx, double* dy, void* stream);
+/* host threads of the staging copy pool */
+int qdot_b200_host_copy_threads(void);
 /* host x, y: allocates device buffers, copies in, runs, copies the result out */
 int qdot_b200_dot_host(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
                        qdot_result* out, qdot_bin* bins, int32_t max_bins);

@@ -98,6 +98,8 @@ SIGNATURES = {
     "qdot_b200_exact_finalize": (_I, [_P, _P]),
     "qdot_b200_exact_fetch": (_I, [_P, ctypes.POINTER(QdotExactResult), _P]),
     "qdot_b200_vec_update": (_I, [_I64, _I, _P, ctypes.c_double, _P, _P, _P]),
+    "qdot_b200_pass1_host": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _I64, _P, _P, _P, _P]),
+    "qdot_b200_host_copy_threads": (_I, []),
     "qdot_b200_generate": (_I, [_I, ctypes.c_double, ctypes.c_uint64, _I64, _I64, _P, _P, _P]),
     "qdot_b200_order_scratch_bytes": (ctypes.c_size_t, [_I64, ctypes.c_int32]),
     "qdot_b200_bin_order": (_I, [_P, _P, _I64, _I, _P, ctypes.c_int32, _P, _P, _P, _P, ctypes.c_size_t, _P]),

@@ -19,7 +19,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libqdot_b200.so")
-SOURCES = ["qdot_kernels.cu", "qdot_capi.cu", "qdot_apps.cu", "qdot_exact.cu", "qdot_order.cu", "qdot_gen.cu"]
+SOURCES = ["qdot_kernels.cu", "qdot_capi.cu", "qdot_apps.cu", "qdot_exact.cu", "qdot_order.cu", "qdot_gen.cu", "qdot_host.cu"]
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) if os.path.isdir(CSRC) else []
 
 NVCC_FLAGS = [

@@ -381,20 +381,15 @@ struct HostPath {
     double* dy = nullptr;
     int64_t cap = 0;
     void* ws = nullptr;
-    cudaStream_t cs = nullptr, ks = nullptr;
-    std::vector<cudaEvent_t> evs;
+    cudaStream_t ks = nullptr;
     void release() {
-        for (auto ev : evs) cudaEventDestroy(ev);
-        evs.clear();
-        if (cs) cudaStreamDestroy(cs);
         if (ks) cudaStreamDestroy(ks);
         cudaFree(dx); cudaFree(dy); cudaFree(ws);
-        dx = dy = nullptr; ws = nullptr; cs = ks = nullptr; cap = 0;
+        dx = dy = nullptr; ws = nullptr; ks = nullptr; cap = 0;
     }
     ~HostPath() { release(); }
 };
 thread_local HostPath g_host;
-constexpr int64_t HOST_CHUNK = 1ll << 22;   // elements per overlapped chunk
 }  // namespace
 
 int qdot_b200_dot_host(const double* hx, const double* hy, int64_t n, int norm, const qdot_config* cfg,
@@ -417,40 +412,19 @@ int qdot_b200_dot_host(const double* hx, const double* hy, int64_t n, int norm, 
         H.cap = nb;
     }
     if (!H.ws) QD_CHECK(cudaMalloc(&H.ws, WS_BYTES), "malloc ws");
-    if (!H.cs) QD_CHECK(cudaStreamCreateWithFlags(&H.cs, cudaStreamNonBlocking), "stream");
     if (!H.ks) QD_CHECK(cudaStreamCreateWithFlags(&H.ks, cudaStreamNonBlocking), "stream");
-    const int64_t nchunks = (n + HOST_CHUNK - 1) / HOST_CHUNK;
-    while ((int64_t)H.evs.size() < nchunks) {
-        cudaEvent_t ev;
-        QD_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
-        H.evs.push_back(ev);
-    }
     double *dx = H.dx, *dy = H.dy;
     void* ws = H.ws;
-    cudaStream_t cs = H.cs, ks = H.ks;
+    cudaStream_t ks = H.ks;
     int rc = QDOT_OK;
     if ((rc = qdot_b200_begin(ws, ks))) return rc;
-    // the copy stream starts after the previous call's kernels are done with the buffers
-    if (!H.evs.empty()) {
-        QD_CHECK(cudaEventRecord(H.evs[0], ks), "event");
-        QD_CHECK(cudaStreamWaitEvent(cs, H.evs[0], 0), "wait");
-    }
-    // copy chunk c on the copy stream while pass 1 consumes chunk c-1
-    for (int64_t c = 0; c < nchunks; ++c) {
-        const int64_t off = c * HOST_CHUNK;
-        const int64_t len = n - off < HOST_CHUNK ? n - off : HOST_CHUNK;
-        QD_CHECK(cudaMemcpyAsync(dx + off, hx + off, sizeof(double) * len, cudaMemcpyHostToDevice, cs), "H2D x");
-        if (!norm)
-            QD_CHECK(cudaMemcpyAsync(dy + off, hy + off, sizeof(double) * len, cudaMemcpyHostToDevice, cs), "H2D y");
-        QD_CHECK(cudaEventRecord(H.evs[c], cs), "event");
-        QD_CHECK(cudaStreamWaitEvent(ks, H.evs[c], 0), "wait");
-        if ((rc = qdot_b200_pass1(dx + off, norm ? nullptr : dy + off, len, norm, cfg, n, ws, ks))) break;
-    }
+    // chunked H2D (pageable inputs through the library's pinned staging ring)
+    // overlapped with pass 1 (qdot_host.cu)
+    rc = qdot_b200_pass1_host(hx, hy, n, norm, cfg, n, ws, dx, dy, ks);
     if (!rc) rc = qdot_b200_score_finalize(ws, n, cfg, ks);
     if (!rc) rc = qdot_b200_pass2_finalize(dx, norm ? nullptr : dy, n, norm, ws, ks);
     if (!rc) rc = qdot_b200_fetch(ws, out, bins, max_bins, ks);
     cudaStreamSynchronize(ks);
-    cudaStreamSynchronize(cs);
     return rc;
 }
 

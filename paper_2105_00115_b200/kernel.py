@@ -329,9 +329,9 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
 
 
 # host inputs at least this long are streamed to the device in chunks that
-# pass 1 consumes while the next chunk is in flight (copy / compute overlap)
+# pass 1 consumes while the next chunk is in flight (copy / compute overlap;
+# pageable memory through the library's pinned staging ring, csrc/qdot_host.cu)
 PIPELINE_MIN = 1 << 22
-PIPELINE_CHUNK = 1 << 23
 
 
 def _host_vector(a):
@@ -352,33 +352,18 @@ def _host_vector(a):
 
 
 def h2d_pass1(xh, yh, norm: bool, c, n_total: int, st, device):
-    """Copy host vectors to new device buffers in PIPELINE_CHUNK pieces on a
-    copy stream while pass 1 (current stream, workspace already begun)
-    consumes each piece as it lands.  Returns the device vectors."""
+    """Copy host vectors (pageable or pinned) into new device buffers chunk by
+    chunk while pass 1 consumes each landed chunk on the current stream
+    (workspace already begun): qdot_b200_pass1_host.  Returns the device vectors."""
     import torch
     n = int(xh.shape[0])
     lib = _lib.load()
-    comp = torch.cuda.current_stream(device)
-    copy = getattr(st, "copy_stream", None)
-    if copy is None:
-        copy = st.copy_stream = torch.cuda.Stream(device)
-    s = comp.cuda_stream
+    s = torch.cuda.current_stream(device).cuda_stream
     xd = torch.empty(n, dtype=torch.float64, device=device)
     yd = xd if norm else torch.empty(n, dtype=torch.float64, device=device)
-    xd.record_stream(copy)
-    yd.record_stream(copy)
-    copy.wait_stream(comp)                      # the buffers are free to overwrite
-    for off in range(0, n, PIPELINE_CHUNK):
-        ln = min(PIPELINE_CHUNK, n - off)
-        with torch.cuda.stream(copy):
-            xd[off:off + ln].copy_(xh[off:off + ln], non_blocking=True)
-            if not norm:
-                yd[off:off + ln].copy_(yh[off:off + ln], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(copy)
-        comp.wait_event(ev)
-        _lib.check(lib.qdot_b200_pass1(xd.data_ptr() + 8 * off, yd.data_ptr() + 8 * off, ln, int(norm),
-                                       ctypes.byref(c), n_total, st.ws_ptr, s), lib)
+    _lib.check(lib.qdot_b200_pass1_host(xh.data_ptr(), xh.data_ptr() if norm else yh.data_ptr(), n, int(norm),
+                                        ctypes.byref(c), n_total, st.ws_ptr, xd.data_ptr(),
+                                        xd.data_ptr() if norm else yd.data_ptr(), s), lib)
     return xd, yd
 
 

@@ -325,7 +325,7 @@ def test_host_inputs_pipelined_equal_device(norm):
     # report must equal the one for the same vectors already on the device
     from paper_2105_00115_b200 import kernel
     rng = np.random.default_rng(77)
-    n = kernel.PIPELINE_MIN + 3 * kernel.PIPELINE_CHUNK // 2 + 12345
+    n = kernel.PIPELINE_MIN + 3 * (1 << 22) // 2 + 12345        # several staging chunks, a ragged tail
     x = rng.standard_normal(n) * np.exp2(rng.integers(-30, 30, n))
     y = x if norm else rng.standard_normal(n)
     cfg = Q.ToleranceConfig(1e-9, Q.SplitMode.PER_BIN)
@@ -339,6 +339,31 @@ def test_host_inputs_pipelined_equal_device(norm):
             assert r.value == d.value and r.counts == d.counts and r.abs_bound == d.abs_bound
             assert [(q.lower, q.upper, q.cardinality, q.precision) for q in r.params.bins] == \
                    [(q.lower, q.upper, q.cardinality, q.precision) for q in d.params.bins]
+
+
+def test_pageable_staging_ring_back_to_back():
+    """numpy inputs of many staging chunks, back-to-back calls with different
+    data (the pinned staging ring is reused across calls: a buffer is refilled
+    only after its previous H2D finished) and the C ABI one-call host path."""
+    import ctypes
+    from paper_2105_00115_b200 import _lib
+    from paper_2105_00115_b200.device import config_struct
+    n = (1 << 24) + 5
+    cfg = Q.ToleranceConfig(1e-8)
+    pairs = [O.gen_normal(n, seed=s) for s in (40, 41, 42)]
+    want = [Q.qdot(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg).value for a, b in pairs]
+    for _ in range(2):
+        assert [Q.qdot(a, b, cfg).value for a, b in pairs] == want
+    lib = _lib.load()
+    c = config_struct(cfg, Q.ExactBinning())
+    res = _lib.QdotResult()
+    bins = (_lib.QdotBin * (_lib.KEYS + 1))()
+    dp = ctypes.POINTER(ctypes.c_double)
+    for (a, b), w in zip(pairs, want):
+        _lib.check(lib.qdot_b200_dot_host(a.ctypes.data_as(dp), b.ctypes.data_as(dp), n, 0, ctypes.byref(c),
+                                          ctypes.byref(res), bins, _lib.KEYS + 1), lib)
+        assert res.value == w
+    assert lib.qdot_b200_host_copy_threads() >= 1
 
 
 @pytest.mark.parametrize("strategy,eps", [("ranged:8", 1e-8), ("ranged:2", 1e-8), ("ranged:8", 1e-4), ("ranged:3", 1e-6)])
