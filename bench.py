@@ -107,16 +107,62 @@ def profile_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons; only samples received inside the
-    timed window [mark_start, mark_stop] are kept."""
+    """SM clocks + throttle reasons sampled DURING the timed window.
+
+    NVML (the library nvidia-smi reads) polled every ~2 ms from a thread, so
+    even the driver's short burst (K steps of < 1 ms) gets samples; only
+    samples taken inside [mark_start, mark_stop] are kept.  Falls back to
+    `nvidia-smi -lms 50` when NVML is unavailable."""
+
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []                  # (t, sm_mhz, reasons) from NVML
         self.t0 = self.t1 = None
+        self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.idx)
+            bus = "%08X:%02X:%02X.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.idx)
 
     def start(self):
+        try:
+            pynvml, h = self._nvml_handle()
+            self.nvml = (pynvml, h)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        mhz = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.perf_counter(), mhz,
+                                             tuple(nm for nm, b in bits.items() if r & b)))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -139,33 +185,45 @@ class ClockSampler:
     def mark_stop(self):
         self.t1 = time.perf_counter()
 
+    def _inside(self, t):
+        return self.t0 is None or (self.t0 <= t <= (self.t1 or t))
+
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.12)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sms, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for t, ln in self.lines:
-            if self.t0 is not None and not (self.t0 <= t <= (self.t1 or t) + 0.06):
-                continue
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
+        sms, mx, reasons = [], self.max_mhz, set()
+        if self.nvml is not None:
+            self._stop.set()
+            self.t.join(timeout=1)
+            for t, mhz, rs in self.samples:
+                if self._inside(t):
+                    sms.append(mhz)
+                    reasons.update(rs)
+            src = "nvml"
+        elif self.proc is not None:
+            time.sleep(0.12)
+            self.proc.terminate()
             try:
-                sms.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            for t, ln in self.lines:
+                if not (self.t0 is None or self.t0 <= t <= (self.t1 or t) + 0.06):
+                    continue
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sms.append(float(parts[0]))
+                    mx = float(parts[1])
+                except ValueError:
+                    continue
+                for nm, v in zip(self.NAMES, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+            src = "nvidia-smi"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sms)}
+                "reasons": sorted(reasons), "samples": len(sms), "source": src}
 
 
 REF_DIR = os.path.join(ROOT, "baseline", "_ref")
