@@ -188,16 +188,24 @@ int qdot_b200_dot_host(const double* x, const double* y, int64_t n, int norm, co
 #define QDOT_BATCH_OVERFLOW 2    /* OverflowError for that row                               */
 #define QDOT_BATCH_EPS 4         /* floor_log2(eps_eff) ValueError                           */
 #define QDOT_BATCH_GENERAL 8     /* not finished by the fused kernel: recompute the row with
-                                    the single-vector path (non-exact strategy, keys spread
-                                    over > 64 exponents, DOUBLE overflow, len > 65536, ...)  */
+                                    the single-vector path (keys spread over > 64
+                                    exponents, DOUBLE overflow, len > 65536, ...)            */
 #define QDOT_BATCH_EARLY 16      /* early-terminated row                                     */
 #define QDOT_BATCH_HALF_ORDER 32 /* a HALF bin the reference sums order-sensitively          */
+#define QDOT_BATCH_MAX_BINS 64   /* row stride of the per-row bin tables                     */
 /* rows x len row-major (row stride ld >= len elements), one warp per row, one
  * HBM pass.  Device outputs: values[rows]; counts[4*rows] (PERFORATE incl.
  * zeros, HALF, SINGLE, DOUBLE); info[4*rows] = {n_bins, e_min, e_max, status}.
  * Equivalent to qdot(X[r], Y[r], cfg) per row (kernel.py:179-240). */
 int qdot_b200_batched(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, int norm,
                       const qdot_config* cfg, double* values, int64_t* counts, int32_t* info, void* stream);
+/* the same, also writing each row's bin table (the reference's
+ * QdotReport.params.bins per row, kernel.py:62-72): row r's info[4r] bins at
+ * bins[r * QDOT_BATCH_MAX_BINS ...] (device memory, rows * 64 entries); rows
+ * flagged QDOT_BATCH_GENERAL / _HALF_ORDER have no table (the caller reruns them). */
+int qdot_b200_batched_bins(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, int norm,
+                           const qdot_config* cfg, double* values, int64_t* counts, int32_t* info, qdot_bin* bins,
+                           void* stream);
 
 /* --- lazy Bin.indices support (binning.py:174) ------------------------------- */
 /* write the bin id of every element (-1 for exact-zero products) given a

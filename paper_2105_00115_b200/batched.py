@@ -8,12 +8,18 @@ has no batched entry point (SURVEY.md §7.1 adds it; BASELINE.json configs[3]
 is 65,536 dots of length 4,096); its oracle is a per-row loop of qdot.
 
 One warp per row streams the row once and finishes the whole pipeline in
-registers and shared memory (csrc/qdot_batched.cuh).  Rows the fused kernel
-flags QDOT_BATCH_GENERAL (non-exact strategies, exponents spread over more
-than 64 values, DOUBLE overflow, ...) are recomputed here through the
+registers and shared memory (csrc/qdot_batched.cuh); ranged and split
+strategies too (a second pass over the row for the HALF / SINGLE members whose
+products depend on the partition).  Rows the fused kernel flags
+QDOT_BATCH_GENERAL (exponents spread over more than 64 values, DOUBLE
+overflow, rows longer than 2^16, ...) are recomputed here through the
 single-vector device pipeline, so results never depend on that split; so are
 rows with a HALF bin whose fp32 sequential sum is order-sensitive (that
 pipeline replays it in index order, qdot_b200_half_ordered).
+
+bins=True also returns every row's bin table (QdotReport.params.bins per row:
+lower, upper, cardinality, score, precision, value), from the kernel
+(qdot_b200_batched_bins) or, for recomputed rows, from the single-vector run.
 """
 
 from __future__ import annotations
@@ -30,6 +36,13 @@ from .kernel import _raise_status, run_device
 from .scoring import LEVELS_ASC, PrecisionLevel, ToleranceConfig
 
 GENERAL, NONFINITE, OVERFLOW, EPS, EARLY, HALF_ORDER = 8, 1, 2, 4, 16, 32
+MAX_BINS = 64            # QDOT_BATCH_MAX_BINS: row stride of the device bin tables
+
+# qdot_bin (include/qdot_b200.h) as a numpy record
+BIN_DTYPE = np.dtype([("lower", "<i8"), ("upper", "<i8"), ("cardinality", "<i8"), ("score", "<i8"),
+                      ("precision", "<i4"), ("first_key", "<i4"), ("last_key", "<i4"), ("flags", "<i4"),
+                      ("value", "<f8")])
+assert BIN_DTYPE.itemsize == ctypes.sizeof(_lib.QdotBin)
 
 
 @dataclass
@@ -42,9 +55,19 @@ class BatchedReport:
     early_terminated: np.ndarray  # bool[rows]
     half_order_sensitive: np.ndarray  # bool[rows]
     general_rows: np.ndarray = field(default_factory=lambda: np.empty(0, dtype=np.int64))
+    bin_table: np.ndarray = None          # BIN_DTYPE[rows, MAX_BINS] (bins=True)
+    _rerun_bins: dict = field(default_factory=dict, repr=False)
 
     def count(self, level: PrecisionLevel) -> np.ndarray:
         return self.counts[:, LEVELS_ASC.index(level)]
+
+    def row_bins(self, r: int) -> np.ndarray:
+        """Bin table of row r (BIN_DTYPE records, ascending upper); needs bins=True."""
+        if self.bin_table is None:
+            raise ValueError("qdot_batched(..., bins=True) keeps the bin tables")
+        if r in self._rerun_bins:
+            return self._rerun_bins[r]
+        return self.bin_table[r, :int(self.n_bins[r])]
 
 
 def _as_matrix(A, device):
@@ -66,7 +89,7 @@ def _as_matrix(A, device):
     return torch.from_numpy(np.ascontiguousarray(a)).to(device)
 
 
-def qdot_batched(X, Y, cfg: ToleranceConfig, strategy: Strategy = None) -> BatchedReport:
+def qdot_batched(X, Y, cfg: ToleranceConfig, strategy: Strategy = None, bins: bool = False) -> BatchedReport:
     """Row-wise qdot of two (rows, length) fp64 matrices (same result as a loop of qdot)."""
     torch = require_cuda()
     if strategy is None:
@@ -93,8 +116,15 @@ def qdot_batched(X, Y, cfg: ToleranceConfig, strategy: Strategy = None) -> Batch
     values = torch.empty(max(rows, 1), dtype=torch.float64, device=device)
     counts = torch.empty((max(rows, 1), 4), dtype=torch.int64, device=device)
     info = torch.empty((max(rows, 1), 4), dtype=torch.int32, device=device)
-    _lib.check(lib.qdot_b200_batched(Xd.data_ptr(), Yd.data_ptr(), rows, length, ld, int(norm), ctypes.byref(c),
-                                     values.data_ptr(), counts.data_ptr(), info.data_ptr(), s), lib)
+    if bins:
+        btab = torch.empty(max(rows, 1) * MAX_BINS * BIN_DTYPE.itemsize, dtype=torch.uint8, device=device)
+        _lib.check(lib.qdot_b200_batched_bins(Xd.data_ptr(), Yd.data_ptr(), rows, length, ld, int(norm),
+                                              ctypes.byref(c), values.data_ptr(), counts.data_ptr(),
+                                              info.data_ptr(), btab.data_ptr(), s), lib)
+    else:
+        _lib.check(lib.qdot_b200_batched(Xd.data_ptr(), Yd.data_ptr(), rows, length, ld, int(norm),
+                                         ctypes.byref(c), values.data_ptr(), counts.data_ptr(), info.data_ptr(),
+                                         s), lib)
     v = values[:rows].cpu().numpy()
     cn = counts[:rows].cpu().numpy()
     inf = info[:rows].cpu().numpy()
@@ -107,6 +137,9 @@ def qdot_batched(X, Y, cfg: ToleranceConfig, strategy: Strategy = None) -> Batch
     rep = BatchedReport(values=v.copy(), counts=cn.copy(), n_bins=inf[:, 0].copy(), e_min=inf[:, 1].copy(),
                         e_max=inf[:, 2].copy(), early_terminated=(st & EARLY) != 0,
                         half_order_sensitive=(st & HALF_ORDER) != 0, general_rows=general)
+    if bins:
+        rep.bin_table = btab[:rows * MAX_BINS * BIN_DTYPE.itemsize].cpu().numpy().view(BIN_DTYPE).reshape(
+            rows, MAX_BINS)
     if np.any((st & OVERFLOW) & ~(st & GENERAL)):
         raise OverflowError("math range error")
     if np.any((st & EPS) & ~(st & GENERAL)):
@@ -114,7 +147,7 @@ def qdot_batched(X, Y, cfg: ToleranceConfig, strategy: Strategy = None) -> Batch
     for r in general.tolist():
         xr = Xd[r]
         yr = xr if norm else Yd[r]
-        res, _, _ = run_device(xr, yr, length, norm, cfg, strategy, timing=False)
+        res, rb, _ = run_device(xr, yr, length, norm, cfg, strategy, timing=False)
         _raise_status(res)
         rep.values[r] = res.value
         rep.counts[r] = [res.counts[i] for i in range(4)]
@@ -123,4 +156,8 @@ def qdot_batched(X, Y, cfg: ToleranceConfig, strategy: Strategy = None) -> Batch
         rep.e_max[r] = res.e_max
         rep.early_terminated[r] = bool(res.early_terminated)
         rep.half_order_sensitive[r] = bool(res.half_order_sensitive)
+        if bins:
+            nb = int(res.n_bins)
+            rep._rerun_bins[r] = np.frombuffer(ctypes.string_at(ctypes.addressof(rb), nb * BIN_DTYPE.itemsize),
+                                               dtype=BIN_DTYPE).copy() if nb else np.empty(0, dtype=BIN_DTYPE)
     return rep

@@ -9,10 +9,19 @@
 // (scoring.py:96-216), per-bin rounding (emulate.py:116-154) and the Neumaier
 // fold (emulate.py:157-163) -- all inside the warp, no inter-row traffic.
 //
-// Rows the fast kernel cannot finish exactly are flagged BS_GENERAL and
-// re-run by the host through the single-vector pipeline: strategies other
-// than exact binning, keys spread beyond the 64-key window, DOUBLE product
-// overflow, early termination below input_mu 52, rows longer than 2^16.
+// Ranged and split strategies (b_row_general): the partition, scores and
+// precisions come from the same per-key counts; a HALF / SINGLE bin whose
+// upper exceeds a member's key needs that member's partition-dependent
+// product, so the warp streams its row a second time for those keys only
+// (k_pass2's scaled_units), then rounds every bin like bin_value.
+//
+// Rows the kernel cannot finish exactly are flagged BS_GENERAL and re-run by
+// the host through the single-vector pipeline: keys spread beyond the 64-key
+// window, DOUBLE product overflow, early termination below input_mu 52, rows
+// longer than 2^16.
+//
+// Per-row bin tables (optional, qdot_b200_batched_bins): row r's bins at
+// bins[r * QDOT_BATCH_MAX_BINS ...], info[4r] of them.
 
 constexpr int BW = 16;            // per-lane private window (keys)
 constexpr int BCW = 64;           // per-warp limb table window (keys)
@@ -40,7 +49,9 @@ struct BParams {
     int32_t input_mu;
     int32_t strategy;
     int32_t norm;
+    int64_t strategy_param;      // ranged width / split levels
 };
+static_assert(BCW == QDOT_BATCH_MAX_BINS, "bin table stride");
 
 // flush per-lane slots into the warp's limb table (all lanes, warp-synchronous).
 // Transposed: lane L sums key (L & 15) over lanes 16*(L >> 4) .. +15 (staggered
@@ -233,10 +244,286 @@ __device__ __forceinline__ void b_load_tail(const double* __restrict__ xr, const
     }
 }
 
-template <bool NORM, bool VEC>
+// the per-key totals of the warp's limb table (table index j, key cbase + j)
+__device__ __forceinline__ __int128 bw_d(const BWarp& W, int j) {
+    return (__int128)W.c[1][j] + ((__int128)W.c[2][j] << 14) + ((__int128)W.c[3][j] << 28) +
+           ((__int128)(int32_t)W.c[4][j] << 42);
+}
+__device__ __forceinline__ long long bw_s(const BWarp& W, int j) {
+    return (long long)W.c[5][j] + ((long long)(int32_t)W.c[6][j] << 14);
+}
+__device__ __forceinline__ long long bw_h(const BWarp& W, int j) { return (long long)(int32_t)W.c[7][j]; }
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// scratch of b_row_general inside the warp's private slots (zero between rows;
+// re-zeroed before it returns)
+constexpr int BG_SLOTS = 16;      // pass-2 keys with per-lane accumulators (more: shared atomics)
+struct BGenScratch {
+    uint32_t off[BCW + 4];        // exclusive prefix of the key counts, off[BCW] = nnz
+    uint32_t info[BCW];           // pass-2 descriptor per key (P2_NEED | P2_HALF | delta)
+    uint32_t p2lo[BCW], p2hi[BCW];// pass-2 units of keys without a slot: lo 14 bits + signed rest
+    long long p2[BCW];            // pass-2 sum per key
+    double val[BCW];              // bin values in bin order (for the fold)
+    int slot[BCW];                // per-lane accumulator slot of a pass-2 key, or -1
+    long long pacc[BG_SLOTS][32]; // per-lane pass-2 accumulators (no atomics)
+};
+static_assert(sizeof(BGenScratch) <= sizeof(ulonglong2) * BW * 32, "scratch fits the private slots");
+
+// Ranged / split rows (not early-terminated) of one warp: k_score's partition
+// (binning.py:202-274), scores / precisions (scoring.py:96-123, 181-199),
+// k_pass2's scaled products (emulate.py:137-147) for keys below their bin's
+// upper, bin_value's rounding (emulate.py:116-154) and the Neumaier fold
+// (emulate.py:157-163).  Lane-local results: cnt_p (summed by the caller).
+template <bool NORM>
+__device__ __noinline__ void b_row_general(BWarp& W, int lane, int cbase, const BParams& prm,
+                                           const double* __restrict__ xr, const double* __restrict__ yr,
+                                           int64_t len, uint32_t& st, double& value, long long (&cnt_p)[4],
+                                           int& nbins, int& emin, int& emax, qdot_bin* __restrict__ bout) {
+    BGenScratch& G = *reinterpret_cast<BGenScratch*>(W.priv);
+    const uint32_t c0 = W.c[0][lane], c1 = W.c[0][lane + 32];
+    const unsigned long long P = (unsigned long long)__ballot_sync(0xffffffffu, c0 != 0) |
+                                 ((unsigned long long)__ballot_sync(0xffffffffu, c1 != 0) << 32);
+    value = 0.0;
+    nbins = 0;
+    if (!P) return;
+    const int jmin = __ffsll((long long)P) - 1, jmax = 63 - __clzll((long long)P);
+    emin = cbase + jmin - KOFF;
+    emax = cbase + jmax - KOFF;
+    {
+        const uint32_t i0 = warp_incl_scan(c0, lane), i1 = warp_incl_scan(c1, lane);
+        const uint32_t t0 = __shfl_sync(0xffffffffu, i0, 31);
+        G.off[lane] = i0 - c0;
+        G.off[lane + 32] = t0 + i1 - c1;
+        if (lane == 31) G.off[BCW] = t0 + i1;
+        G.info[lane] = 0u;
+        G.info[lane + 32] = 0u;
+    }
+    __syncwarp();
+    const unsigned long long nnz = G.off[BCW];
+    // ---- bin starts (binning.py:202-222 ranged, 224-274 split)
+    unsigned long long S = 0ull;
+    if (prm.strategy == QDOT_STRATEGY_RANGED) {
+        const long long w = prm.strategy_param;
+        bool f[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            f[h] = false;
+            if ((P >> j) & 1ull) {
+                const int gs = jmin + (int)(((long long)(j - jmin) / w) * w);
+                const unsigned long long below = ((1ull << j) - 1ull) ^ ((1ull << gs) - 1ull);   // keys [gs, j)
+                f[h] = (P & below) == 0ull;
+            }
+        }
+        S = (unsigned long long)__ballot_sync(0xffffffffu, f[0]) |
+            ((unsigned long long)__ballot_sync(0xffffffffu, f[1]) << 32);
+    } else {
+        long long levels = prm.strategy_param;
+        const unsigned long long t = nnz > 1 ? nnz - 1 : 0;
+        const int bl = t ? 64 - __clzll((long long)t) : 0;
+        if (levels > bl) levels = bl;                                              // binning.py:235
+        uint32_t nx[2] = {0u, 0u};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            if (!((P >> j) & 1ull)) continue;
+            const unsigned long long a = G.off[j], b = a + W.c[0][j];
+            if (b < nnz && split_boundary_in(nnz, (int)levels, a, b)) {             // cut after key j
+                const unsigned long long rest = j == 63 ? 0ull : (P & ~((2ull << j) - 1ull));
+                const int nj = __ffsll((long long)rest) - 1;                         // next present key
+                nx[nj >> 5] |= 1u << (nj & 31);
+            }
+        }
+        S = (unsigned long long)__reduce_or_sync(0xffffffffu, nx[0]) |
+            ((unsigned long long)__reduce_or_sync(0xffffffffu, nx[1]) << 32) | (1ull << jmin);
+    }
+    nbins = __popcll(S);
+    const double eps_eff = prm.split == 1 ? __ddiv_rn(prm.epsilon, (double)nbins) : prm.epsilon;   // scoring.py:192
+    bool okf = true;
+    const long long fl = floor_log2_d(eps_eff, &okf);
+    if (!okf) { st |= BS_EPS; return; }
+    // ---- per bin (the lane owning its first key): interval, score, precision; pass-2 keys
+    long long bu[2] = {0, 0}, bl_[2] = {0, 0}, bm[2] = {0, 0}, bsc[2] = {0, 0};
+    int bpr[2] = {0, 0}, bidx[2] = {-1, -1}, bl2[2] = {0, 0};
+    bool need = false;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        if (!((S >> j) & 1ull)) continue;
+        const int b = __popcll(S & ((1ull << j) - 1ull));
+        const unsigned long long rest = j == 63 ? 0ull : (S & ~((2ull << j) - 1ull));
+        const int nf = rest ? __ffsll((long long)rest) - 1 : BCW;
+        const unsigned long long upto = nf == BCW ? ~0ull : ((1ull << nf) - 1ull);
+        const int l = 63 - __clzll((long long)(P & upto));
+        const long long M = (long long)(G.off[nf] - G.off[j]);
+        long long upper, lower;
+        if (prm.strategy == QDOT_STRATEGY_RANGED) {
+            const long long w = prm.strategy_param;
+            const long long g = (long long)(j - jmin) / w;
+            upper = (long long)emin + (g + 1) * w - 1;
+            lower = upper - w;
+        } else {
+            upper = cbase + l - KOFF;
+            const unsigned long long pb = P & ((1ull << j) - 1ull);
+            lower = pb ? (long long)(cbase + (63 - __clzll((long long)pb)) - KOFF) : (long long)emin - 1;
+        }
+        const unsigned long long mm = (unsigned long long)(M - 1);
+        const long long score = (mm ? 64 - __clzll((long long)mm) : 0) + upper - emax - fl + 1;   // bin_score
+        const int pr = precision_of(score, prm.input_mu);
+        bu[h] = upper; bl_[h] = lower; bm[h] = M; bsc[h] = score; bpr[h] = pr; bidx[h] = b; bl2[h] = l;
+        if (pr == QDOT_HALF || pr == QDOT_SINGLE) {
+            for (int k = j; k <= l; ++k) {
+                if (!((P >> k) & 1ull)) continue;
+                const long long d = upper - (long long)(cbase + k - KOFF);
+                if (d > 0) {
+                    G.info[k] = P2_NEED | (pr == QDOT_HALF ? P2_HALF : 0u) | (uint32_t)(d > P2_DELTA_MAX ? P2_DELTA_MAX : d);
+                    need = true;
+                }
+            }
+        }
+    }
+    // ---- second pass over the row for the keys whose products depend on the partition
+    if (__any_sync(0xffffffffu, need)) {
+        const unsigned long long N = (unsigned long long)__ballot_sync(0xffffffffu, (G.info[lane] & P2_NEED) != 0) |
+                                     ((unsigned long long)__ballot_sync(0xffffffffu, (G.info[lane + 32] & P2_NEED) != 0) << 32);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            const int sl = ((N >> j) & 1ull) ? __popcll(N & ((1ull << j) - 1ull)) : -1;
+            G.slot[j] = sl < BG_SLOTS ? sl : -1;
+            G.p2lo[j] = 0u;
+            G.p2hi[j] = 0u;
+        }
+        for (int sl = 0; sl < BG_SLOTS; ++sl) G.pacc[sl][lane] = 0;
+        __syncwarp();
+        auto elem = [&](double a, double bb) {
+            if (a == 0.0 || bb == 0.0) return;
+            const uint64_t bx = dbits(a), by = dbits(bb);
+            const int j = flexp_bits(bx) + flexp_bits(by) + KOFF - cbase;
+            if ((unsigned)j >= (unsigned)BCW) return;
+            const uint32_t inf = G.info[j];
+            if (!(inf & P2_NEED)) return;
+            long long k = scaled_units(bitsd(mant_bits(bx)), bitsd(mant_bits(by)), inf);
+            if ((bx ^ by) >> 63) k = -k;
+            const int sl = G.slot[j];
+            if (sl >= 0) {
+                G.pacc[sl][lane] += k;
+            } else {
+                atomicAdd(&G.p2lo[j], (uint32_t)((uint64_t)k & 0x3FFFu));
+                atomicAdd(&G.p2hi[j], (uint32_t)(int32_t)(k >> 14));
+            }
+        };
+        const bool vec = ((reinterpret_cast<uintptr_t>(xr) | reinterpret_cast<uintptr_t>(yr)) & 15u) == 0;
+        int64_t i0 = 0;
+        if (vec) {
+            for (; i0 + 64 <= len; i0 += 64) {
+                const double2 a = __ldcs(reinterpret_cast<const double2*>(xr + i0) + lane);
+                const double2 bb = NORM ? a : __ldcs(reinterpret_cast<const double2*>(yr + i0) + lane);
+                elem(a.x, bb.x);
+                elem(a.y, bb.y);
+            }
+        }
+        for (int64_t i = i0 + lane; i < len; i += 32) {
+            const double a = xr[i];
+            elem(a, NORM ? a : yr[i]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            long long v = (long long)G.p2lo[j] + ((long long)(int32_t)G.p2hi[j] << 14);
+            const int sl = G.slot[j];
+            if (sl >= 0)
+                for (int l2 = 0; l2 < 32; ++l2) v += G.pacc[sl][l2];
+            G.p2[j] = v;
+        }
+        __syncwarp();
+    }
+    // ---- bin values (bin_value, emulate.py:116-154)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (bidx[h] < 0) continue;
+        const int f = lane + 32 * h, l = bl2[h];
+        const long long u = bu[h];
+        const int pr = bpr[h];
+        double val = 0.0;
+        int o = 0, hf = 0;
+        if (pr == QDOT_DOUBLE) {
+            if (f == l) val = round_i128(bw_d(W, f), qd_double(cbase + f - KOFF), 52, -1022, 1023, &o);
+            else {
+                BigSum<104> acc;
+                const int lsb = qd_double(cbase + f - KOFF);
+                acc.init(lsb, (qd_double(cbase + l - KOFF) - lsb + 160) / 32 + 2);
+                for (int k = f; k <= l; ++k)
+                    if ((P >> k) & 1ull) acc.add(bw_d(W, k), qd_double(cbase + k - KOFF));
+                val = acc.round(52, -1022, 1023, &o);
+            }
+        } else if (pr != QDOT_PERFORATE) {
+            const bool half = pr == QDOT_HALF;
+            const int mu = half ? 10 : 23;
+            const int qmin_fmt = half ? -24 : -149;
+            auto qs_of = [&](int k) {
+                const long long d = u - (long long)(cbase + k - KOFF);
+                const int dd = d > P2_DELTA_MAX ? P2_DELTA_MAX : (int)d;
+                return -dd - mu > qmin_fmt ? -dd - mu : qmin_fmt;
+            };
+            auto keyval = [&](int k) -> long long {
+                if (G.info[k] & P2_NEED) return G.p2[k];
+                return half ? bw_h(W, k) : bw_s(W, k);
+            };
+            const int lsb = qs_of(f);
+            double mass = 0.0;
+            BigSum<16> acc;
+            acc.init(lsb, (qs_of(l) - lsb + 128) / 32 + 2);
+            for (int k = f; k <= l; ++k) {
+                if (!((P >> k) & 1ull)) continue;
+                const long long d = u - (long long)(cbase + k - KOFF);
+                acc.add((__int128)keyval(k), qs_of(k));
+                mass += (double)W.c[0][k] * pow2d(2 - (int)(d > 2000 ? 2000 : d));
+            }
+            const double a = half ? acc.round(23, -126, 127, &o) : acc.round(52, -1022, 1023, &o);
+            val = ldexp_rn(a, u, &o);                                                  // emulate.py:154
+            if (half && mass > pow2d(24 + lsb)) hf = 1;
+        }
+        if (o) st |= BS_OVERFLOW;
+        if (hf) st |= BS_HALF_ORDER;
+        G.val[bidx[h]] = val;
+        cnt_p[pr] += bm[h];
+        if (bout) {
+            qdot_bin ob;
+            ob.lower = bl_[h]; ob.upper = u; ob.cardinality = bm[h]; ob.score = bsc[h]; ob.precision = pr;
+            ob.first_key = cbase + f; ob.last_key = cbase + l; ob.flags = hf; ob.value = val;
+            bout[bidx[h]] = ob;
+        }
+    }
+    __syncwarp();
+    // ---- Neumaier fold in ascending upper order (emulate.py:157-163)
+    if (lane == 0) {
+        double sm = 0.0, c = 0.0;
+        neumaier_fold(G.val, nbins, sm, c);
+        value = (sm - sm == 0.0) ? __dadd_rn(sm, c) : sm;
+    }
+    value = __shfl_sync(0xffffffffu, value, 0);
+    __syncwarp();
+    // leave the private slots zero for the next row
+    for (int i = lane; i < (int)(sizeof(BGenScratch) / 16); i += 32) W.priv[i] = make_ulonglong2(0ull, 0ull);
+    __syncwarp();
+}
+
+// GEN: ranged / split strategies (b_row_general); the exact-binning
+// instantiation keeps its epilogue in registers
+template <bool NORM, bool VEC, bool GEN>
 __global__ void __launch_bounds__(B_WARPS * 32, 5)
 k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows, int64_t len, int64_t ld,
-          BParams prm, double* __restrict__ values, int64_t* __restrict__ counts, int32_t* __restrict__ info) {
+          BParams prm, double* __restrict__ values, int64_t* __restrict__ counts, int32_t* __restrict__ info,
+          qdot_bin* __restrict__ bins) {
     __shared__ BWarp warps[B_WARPS];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     BWarp& W = warps[wid];
@@ -251,7 +538,7 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
         const double* xn = has_next ? X + (r + rstride) * ld : nullptr;
         const double* yn = has_next ? (NORM ? xn : Y + (r + rstride) * ld) : nullptr;
         uint32_t st = 0, zc = 0;
-        if (prm.strategy != QDOT_STRATEGY_EXACT || len > B_MAXLEN) st |= BS_GENERAL;
+        if (len > B_MAXLEN) st |= BS_GENERAL;
         // ---- first warp iteration: doubles as the sample that places the windows
         double xa[4], ya[4], xb[4], yb[4];
         bool ok0[4] = {true, true, true, true};
@@ -343,6 +630,7 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
         double value = 0.0;
         long long cnt_p[4] = {0, 0, 0, 0};
         int nbins = 0, emin = 0, emax = 0;
+        qdot_bin* __restrict__ bout = bins ? bins + r * (int64_t)BCW : nullptr;
         if (!(st & (BS_GENERAL | BS_NONFINITE))) {
             // ---- per-key totals: lane owns table entries j = lane and lane + 32
             uint32_t cnt[2];
@@ -384,7 +672,16 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
                     int ovf = 0;
                     if (pr == QDOT_DOUBLE) value = b_early_double(nullptr, jmin, jmax, cbase, lane, D[0], D[1], cnt[0], cnt[1], &ovf);
                     else if (pr != QDOT_PERFORATE) st |= BS_GENERAL;
+                    if (ovf) st |= BS_OVERFLOW;
                     if (lane == 0) cnt_p[pr] += nnz;
+                    if (bout && lane == 0) {
+                        qdot_bin ob;
+                        ob.lower = emin - 1; ob.upper = emax; ob.cardinality = nnz; ob.score = sc; ob.precision = pr;
+                        ob.first_key = cbase + jmin; ob.last_key = cbase + jmax; ob.flags = 0; ob.value = value;
+                        bout[0] = ob;
+                    }
+                } else if (GEN) {
+                    b_row_general<NORM>(W, lane, cbase, prm, xr, yr, len, st, value, cnt_p, nbins, emin, emax, bout);
                 } else {
                     double eps_eff = prm.split == 1 ? __ddiv_rn(prm.epsilon, (double)nbins) : prm.epsilon;
                     long long fl = floor_log2_d(eps_eff, &okf);
@@ -398,17 +695,25 @@ k_batched(const double* __restrict__ X, const double* __restrict__ Y, int64_t ro
                         unsigned long long mm = cnt[h] - 1;
                         long long sc = (mm ? 64 - __clzll((long long)mm) : 0) + e - emax - fl + 1;   // bin_score
                         pr[h] = precision_of(sc, prm.input_mu);
-                        int ovf = 0;
+                        int ovf = 0, hf = 0;
                         if (pr[h] == QDOT_DOUBLE) {
                             val[h] = round_i128(D[h], qd_double(e), 52, -1022, 1023, &ovf);
                         } else if (pr[h] == QDOT_SINGLE) {
                             val[h] = ldexp_rn(round_i128((__int128)S[h], -23, 52, -1022, 1023, &ovf), e, &ovf);
                         } else if (pr[h] == QDOT_HALF) {
                             val[h] = ldexp_rn(round_i128((__int128)H[h], -10, 23, -126, 127, &ovf), e, &ovf);
-                            if ((double)cnt[h] * 4.0 > 16384.0) st |= BS_HALF_ORDER;
+                            if ((double)cnt[h] * 4.0 > 16384.0) { st |= BS_HALF_ORDER; hf = 1; }
                         }
                         if (ovf) st |= BS_OVERFLOW;
                         cnt_p[pr[h]] += cnt[h];
+                        if (bout) {
+                            const int b = h ? __popc(pres0) + __popc(pres1 & ((1u << lane) - 1u))
+                                            : __popc(pres0 & ((1u << lane) - 1u));
+                            qdot_bin ob;
+                            ob.lower = e - 1; ob.upper = e; ob.cardinality = cnt[h]; ob.score = sc; ob.precision = pr[h];
+                            ob.first_key = e + KOFF; ob.last_key = e + KOFF; ob.flags = hf; ob.value = val[h];
+                            bout[b] = ob;
+                        }
                     }
                     // Neumaier fold over bins in ascending key order (emulate.py:157-163)
                     double s = 0.0, c = 0.0;

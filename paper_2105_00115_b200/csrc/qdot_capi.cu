@@ -442,8 +442,21 @@ int qdot_b200_batched(const double* X, const double* Y, int64_t rows, int64_t le
     if (v) return v;
     if (rows < 0 || len < 0 || ld < len || (rows > 0 && (!X || (!norm && !Y) || !values || !counts || !info)))
         return QDOT_ERR_ARG;
-    QD_CHECK(launch_batched(X, Y, rows, len, ld, norm != 0, *cfg, values, counts, info,
+    QD_CHECK(launch_batched(X, Y, rows, len, ld, norm != 0, *cfg, values, counts, info, nullptr,
                             static_cast<cudaStream_t>(stream)), "batched");
+    return QDOT_OK;
+}
+
+int qdot_b200_batched_bins(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, int norm,
+                           const qdot_config* cfg, double* values, int64_t* counts, int32_t* info, qdot_bin* bins,
+                           void* stream) {
+    int v = validate(cfg);
+    if (v) return v;
+    if (rows < 0 || len < 0 || ld < len ||
+        (rows > 0 && (!X || (!norm && !Y) || !values || !counts || !info || !bins)))
+        return QDOT_ERR_ARG;
+    QD_CHECK(launch_batched(X, Y, rows, len, ld, norm != 0, *cfg, values, counts, info, bins,
+                            static_cast<cudaStream_t>(stream)), "batched_bins");
     return QDOT_OK;
 }
 

@@ -1020,13 +1020,22 @@ cudaError_t launch_publish(const void* block, int nbytes, void* host_dev, uint32
     return cudaGetLastError();
 }
 
-template <bool NORM, bool VEC>
+template <bool NORM, bool VEC, bool GEN>
 static cudaError_t launch_batched_t(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld,
                                     const BParams& prm, double* values, int64_t* counts, int32_t* info,
-                                    cudaStream_t st);
+                                    qdot_bin* bins, cudaStream_t st);
+template <bool NORM, bool VEC>
+static cudaError_t launch_batched_g(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld,
+                                    const BParams& prm, double* values, int64_t* counts, int32_t* info,
+                                    qdot_bin* bins, cudaStream_t st) {
+    if (prm.strategy != QDOT_STRATEGY_EXACT)
+        return launch_batched_t<NORM, VEC, true>(X, Y, rows, len, ld, prm, values, counts, info, bins, st);
+    return launch_batched_t<NORM, VEC, false>(X, Y, rows, len, ld, prm, values, counts, info, bins, st);
+}
 
 cudaError_t launch_batched(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, bool norm,
-                           const qdot_config& cfg, double* values, int64_t* counts, int32_t* info, cudaStream_t st) {
+                           const qdot_config& cfg, double* values, int64_t* counts, int32_t* info, qdot_bin* bins,
+                           cudaStream_t st) {
     if (rows <= 0) return cudaSuccess;
     BParams prm;
     prm.epsilon = cfg.epsilon;
@@ -1034,25 +1043,26 @@ cudaError_t launch_batched(const double* X, const double* Y, int64_t rows, int64
     prm.input_mu = cfg.input_mu;
     prm.strategy = cfg.strategy;
     prm.norm = norm ? 1 : 0;
+    prm.strategy_param = cfg.strategy_param;
     const bool vec = ((ld & 1) == 0) &&
                      ((reinterpret_cast<uintptr_t>(X) | (norm ? 0 : reinterpret_cast<uintptr_t>(Y))) & 15u) == 0;
-    if (norm) return vec ? launch_batched_t<true, true>(X, X, rows, len, ld, prm, values, counts, info, st)
-                         : launch_batched_t<true, false>(X, X, rows, len, ld, prm, values, counts, info, st);
-    return vec ? launch_batched_t<false, true>(X, Y, rows, len, ld, prm, values, counts, info, st)
-               : launch_batched_t<false, false>(X, Y, rows, len, ld, prm, values, counts, info, st);
+    if (norm) return vec ? launch_batched_g<true, true>(X, X, rows, len, ld, prm, values, counts, info, bins, st)
+                         : launch_batched_g<true, false>(X, X, rows, len, ld, prm, values, counts, info, bins, st);
+    return vec ? launch_batched_g<false, true>(X, Y, rows, len, ld, prm, values, counts, info, bins, st)
+               : launch_batched_g<false, false>(X, Y, rows, len, ld, prm, values, counts, info, bins, st);
 }
 
-template <bool NORM, bool VEC>
+template <bool NORM, bool VEC, bool GEN>
 static cudaError_t launch_batched_t(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld,
                                     const BParams& prm, double* values, int64_t* counts, int32_t* info,
-                                    cudaStream_t st) {
-    auto kern = k_batched<NORM, VEC>;
+                                    qdot_bin* bins, cudaStream_t st) {
+    auto kern = k_batched<NORM, VEC, GEN>;
     static KernelDevCache cache;
     const int occ = kernel_occupancy(kern, B_WARPS * 32, 0, cache);
     int64_t grid = (rows + B_WARPS - 1) / B_WARPS;
     int64_t cap = (int64_t)sm_count_cached() * occ;
     if (grid > cap) grid = cap;
-    kern<<<(unsigned)grid, B_WARPS * 32, 0, st>>>(X, Y, rows, len, ld, prm, values, counts, info);
+    kern<<<(unsigned)grid, B_WARPS * 32, 0, st>>>(X, Y, rows, len, ld, prm, values, counts, info, bins);
     return cudaGetLastError();
 }
 

@@ -33,7 +33,8 @@ cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* 
 cudaError_t launch_publish(const void* block, int nbytes, void* host_dev, uint32_t* dev_seq, uint32_t* host_seq_dev,
                            cudaStream_t st);
 cudaError_t launch_batched(const double* X, const double* Y, int64_t rows, int64_t len, int64_t ld, bool norm,
-                           const qdot_config& cfg, double* values, int64_t* counts, int32_t* info, cudaStream_t st);
+                           const qdot_config& cfg, double* values, int64_t* counts, int32_t* info, qdot_bin* bins,
+                           cudaStream_t st);
 cudaError_t launch_bin_ids(const double* x, const double* y, int64_t n, bool norm, const int32_t* lut_bin,
                            int32_t* out, cudaStream_t st);
 

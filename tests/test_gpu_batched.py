@@ -99,13 +99,71 @@ def test_special_rows_and_layouts():
     check_rows(X, X, rep, 1e-7)
 
 
-def test_non_exact_strategy_goes_general():
+def check_bins(X, Y, rep, eps, split="none", strategy="exact"):
+    """Per-row bin tables bit-equal to the oracle's (lower, upper, cardinality,
+    score, precision, value)."""
+    for r in range(X.shape[0]):
+        o = O.qdot(X[r], Y[r], eps, split, 52, strategy)
+        got = [(int(b["lower"]), int(b["upper"]), int(b["cardinality"]), int(b["score"]), int(b["precision"]),
+                float(b["value"])) for b in rep.row_bins(r)]
+        want = [(b.lower, b.upper, b.cardinality, b.score, b.precision, b.value) for b in o.bins]
+        assert got == want, (r, strategy)
+
+
+@pytest.mark.parametrize("strategy", ["ranged:1", "ranged:2", "ranged:3", "ranged:7", "ranged:40", "split:0",
+                                      "split:1", "split:3", "split:6", "split:12"])
+@pytest.mark.parametrize("eps,split", [(1e-4, "none"), (1e-9, "per-bin"), (1e-1, "none")])
+def test_non_exact_strategies_on_device(strategy, eps, split):
+    """Ranged / split rows finish in the fused kernel (no per-row host loop),
+    bit-exact against the oracle, bin tables included."""
     rng = np.random.default_rng(33)
-    X = rng.standard_normal((6, 512))
-    Y = rng.standard_normal((6, 512))
-    rep = Q.qdot_batched(X, Y, Q.ToleranceConfig(1e-4), strategy=Q.RangedBinning(3))
-    assert len(rep.general_rows) == 6
-    check_rows(X, Y, rep, 1e-4, strategy="ranged:3")
+    X = rng.standard_normal((40, 700))
+    Y = rng.standard_normal((40, 700))
+    X[3, ::5] = 0.0
+    X[4] *= np.exp2(rng.integers(-20, 20, 700))          # wider exponent spread
+    X[5, :] = 1.0
+    Y[5, :] = 1.0                                        # early-terminated row
+    st = Q.parse_strategy(strategy)
+    cfg = Q.ToleranceConfig(eps, Q.SplitMode(split))
+    rep = Q.qdot_batched(X, Y, cfg, strategy=st, bins=True)
+    check_rows(X, Y, rep, eps, split, strategy)
+    check_bins(X, Y, rep, eps, split, strategy)
+    # rerun rows: the wide row, and rows with an order-sensitive HALF bin (fp32 replay in index order)
+    assert all(r == 4 or rep.half_order_sensitive[r] for r in rep.general_rows.tolist()), rep.general_rows
+    repn = Q.qdot_batched(X, X, cfg, strategy=st, bins=True)
+    check_rows(X, X, repn, eps, split, strategy)
+    check_bins(X, X, repn, eps, split, strategy)
+
+
+@pytest.mark.parametrize("strategy", ["exact", "ranged:3", "split:5"])
+def test_bin_tables_golden_and_general(strategy):
+    """bins=True on C4 golden rows, mixed special rows and a wide-spread row
+    that reruns on the single-vector path."""
+    names = ["C4_row0", "C4_row1", "C4_row2", "C4_row65535"]
+    cases = {c["name"]: c for c in G.cases() if c["name"] in names}
+    X = np.stack([G.inputs(cases[nm])[0] for nm in names])
+    Y = np.stack([G.inputs(cases[nm])[1] for nm in names])
+    X[2, 0] = 1e300                                      # spread > 64 keys: rerun row
+    rep = Q.qdot_batched(X, Y, Q.ToleranceConfig(1e-6), strategy=Q.parse_strategy(strategy), bins=True)
+    assert 2 in rep.general_rows.tolist()
+    check_rows(X, Y, rep, 1e-6, "none", strategy)
+    check_bins(X, Y, rep, 1e-6, "none", strategy)
+    if strategy == "exact":
+        assert rep.values[0] == 45.36721523563339 and rep.values[3] == 72.77242249700646
+
+
+def test_ranged_c4_shape_no_host_loop():
+    """The former per-row host cliff: 4096 rows x 4096, ranged:3 -- all rows on
+    device (none rerun), values equal to the exact per-row oracle on a sample."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    X = torch.randn(4096, 4096, dtype=torch.float64, device="cuda", generator=g)
+    Y = torch.randn(4096, 4096, dtype=torch.float64, device="cuda", generator=g)
+    rep = Q.qdot_batched(X, Y, Q.ToleranceConfig(1e-6), strategy=Q.RangedBinning(3))
+    assert len(rep.general_rows) == 0
+    Xh, Yh = X[:64].cpu().numpy(), Y[:64].cpu().numpy()
+    sub = Q.qdot_batched(Xh, Yh, Q.ToleranceConfig(1e-6), strategy=Q.RangedBinning(3))
+    assert np.array_equal(sub.values, rep.values[:64])
+    check_rows(Xh, Yh, sub, 1e-6, "none", "ranged:3")
 
 
 def test_errors():
