@@ -385,6 +385,225 @@ k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const u
     finalize_body(A, B, lut_p2, m, res, bins);
 }
 
+
+// =============================================================================
+// score, one warp (single device, keys spanning < 64 exponents: the solver
+// regime).  The same partition / scores / precisions / LUTs / meta as the
+// block path below, from bit masks over the 64 keys [kmin, kmin + 64) (lane
+// owns keys kmin + lane and kmin + lane + 32); when no pass 2 follows, the
+// bin values (bin_value over the global key rows), the fold and the result
+// header too.  Saves the block path's ~15 barrier phases per call.
+// =============================================================================
+constexpr int SW_KEYS = 64;
+
+__device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* __restrict__ lut_bin,
+                           uint32_t* __restrict__ lut_p2, ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res,
+                           qdot_bin* __restrict__ bins, int64_t n_total, const qdot_config& cfg, int kmin, int kmax,
+                           unsigned long long ts0, long long a_nonfinite, long long a_zero, long long a_listovf,
+                           double* sval, long long* bup, signed char* bprec) {
+    const int lane = threadIdx.x & 31;
+    long long c[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int k = kmin + lane + 32 * h;
+        c[h] = (k <= kmax) ? A[A_CNT + k] : 0;
+    }
+    const unsigned long long P = (unsigned long long)__ballot_sync(0xffffffffu, c[0] != 0) |
+                                 ((unsigned long long)__ballot_sync(0xffffffffu, c[1] != 0) << 32);
+    // exclusive prefix of the counts: off(j) for the lane's keys, nnz
+    unsigned long long i0 = (unsigned long long)c[0], i1 = (unsigned long long)c[1];
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t0 = __shfl_up_sync(0xffffffffu, i0, o), t1 = __shfl_up_sync(0xffffffffu, i1, o);
+        if (lane >= o) { i0 += t0; i1 += t1; }
+    }
+    const unsigned long long tot0 = __shfl_sync(0xffffffffu, i0, 31);
+    const unsigned long long nnz = tot0 + __shfl_sync(0xffffffffu, i1, 31);
+    const unsigned long long off[2] = {i0 - (unsigned long long)c[0], tot0 + i1 - (unsigned long long)c[1]};
+    auto off_of = [&](int j) -> unsigned long long {     // exclusive prefix at key kmin + j (j <= 64)
+        // every lane supplies both halves: lanes may ask for different ones
+        const unsigned long long v0 = __shfl_sync(0xffffffffu, off[0], j & 31);
+        const unsigned long long v1 = __shfl_sync(0xffffffffu, off[1], j & 31);
+        return j >= SW_KEYS ? nnz : (j < 32 ? v0 : v1);
+    };
+    int status = a_nonfinite ? QDOT_ERR_NONFINITE : QDOT_OK;                   // floatbits.py:70
+    bool ok = true;
+    const long long fle = floor_log2_d(cfg.epsilon, &ok);
+    if (!ok && status == QDOT_OK) status = QDOT_ERR_EPS;
+    int early = 0;
+    if (ok) {                                                                  // scoring.py:126-136
+        const int mu_hat = cfg.input_mu == 52 ? 23 : (cfg.input_mu == 23 ? 10 : 0);
+        early = (long long)(kmax - kmin) <= (-fle - mu_hat);
+    }
+    // ---- bin starts (bit j: key kmin + j starts a bin)
+    const int jmin = 0, jmax = kmax - kmin;
+    unsigned long long S;
+    const int strategy = cfg.strategy;
+    if (early) {
+        S = 1ull;
+    } else if (strategy == QDOT_STRATEGY_EXACT) {
+        S = P;
+    } else if (strategy == QDOT_STRATEGY_RANGED) {
+        const long long w = cfg.strategy_param;
+        bool f[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            f[h] = false;
+            if ((P >> j) & 1ull) {
+                const int gs = jmin + (int)(((long long)(j - jmin) / w) * w);
+                const unsigned long long below = ((1ull << j) - 1ull) ^ ((1ull << gs) - 1ull);
+                f[h] = (P & below) == 0ull;
+            }
+        }
+        S = (unsigned long long)__ballot_sync(0xffffffffu, f[0]) |
+            ((unsigned long long)__ballot_sync(0xffffffffu, f[1]) << 32);
+    } else {
+        long long levels = cfg.strategy_param;                                  // binning.py:235
+        const unsigned long long t = nnz > 1 ? nnz - 1 : 0;
+        const int bl = t ? 64 - __clzll((long long)t) : 0;
+        if (levels > bl) levels = bl;
+        uint32_t nx[2] = {0u, 0u};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            if (!((P >> j) & 1ull)) continue;
+            const unsigned long long a = off[h], b = a + (unsigned long long)c[h];
+            if (b < nnz && split_boundary_in(nnz, (int)levels, a, b)) {
+                const unsigned long long rest = j == 63 ? 0ull : (P & ~((2ull << j) - 1ull));
+                const int nj = __ffsll((long long)rest) - 1;
+                nx[nj >> 5] |= 1u << (nj & 31);
+            }
+        }
+        S = (unsigned long long)__reduce_or_sync(0xffffffffu, nx[0]) |
+            ((unsigned long long)__reduce_or_sync(0xffffffffu, nx[1]) << 32) | 1ull;
+    }
+    const int nb = __popcll(S);
+    const double eps_eff = (cfg.split == 1 && nb) ? __ddiv_rn(cfg.epsilon, (double)nb) : cfg.epsilon;   // scoring.py:192
+    bool okf = true;
+    const long long fl = floor_log2_d(eps_eff, &okf);
+    if (!okf && status == QDOT_OK) status = QDOT_ERR_EPS;
+    const int e_min = kmin - KOFF, e_max = kmax - KOFF;
+    // ---- per bin (lane owning its first key): interval, score, precision, LUT entries
+    int need = 0, priv = 0;
+    qdot_bin ob[2];
+    int bidx[2] = {-1, -1};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        if (!((S >> j) & 1ull)) continue;
+        const int b = __popcll(S & ((1ull << j) - 1ull));
+        const unsigned long long rest = j == 63 ? 0ull : (S & ~((2ull << j) - 1ull));
+        const int nf = rest ? __ffsll((long long)rest) - 1 : SW_KEYS;
+        const unsigned long long upto = nf == SW_KEYS ? ~0ull : ((1ull << nf) - 1ull);
+        const int l = 63 - __clzll((long long)(P & upto));
+        bidx[h] = b;
+        ob[h].first_key = kmin + j;
+        ob[h].last_key = kmin + l;
+        ob[h].flags = 0;
+        ob[h].value = 0.0;
+    }
+    // M needs the prefix at arbitrary keys: shuffles are warp-collective, so
+    // every lane evaluates them for both of its (possible) bins
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        const unsigned long long rest = j == 63 ? 0ull : (S & ~((2ull << j) - 1ull));
+        const int nf = rest ? __ffsll((long long)rest) - 1 : SW_KEYS;
+        const unsigned long long a = off_of(j & 63), b = off_of(nf);
+        if (bidx[h] < 0) continue;
+        const long long M = (long long)(b - a);
+        const int f = ob[h].first_key, l = ob[h].last_key;
+        long long upper, lower;
+        if (early) { lower = e_min - 1; upper = e_max; }
+        else if (strategy == QDOT_STRATEGY_EXACT) { upper = l - KOFF; lower = upper - 1; }
+        else if (strategy == QDOT_STRATEGY_RANGED) {
+            const long long w = cfg.strategy_param;
+            const long long g = (long long)(f - kmin) / w;
+            upper = (long long)e_min + (g + 1) * w - 1;
+            lower = upper - w;
+        } else {
+            upper = l - KOFF;
+            const unsigned long long pb = P & ((1ull << j) - 1ull);
+            lower = pb ? (long long)(kmin + (63 - __clzll((long long)pb)) - KOFF) : (long long)e_min - 1;
+        }
+        const unsigned long long mm = (unsigned long long)(M - 1);
+        const long long score = (mm ? 64 - __clzll((long long)mm) : 0) + upper - e_max - fl + 1;   // bin_score
+        ob[h].lower = lower; ob[h].upper = upper; ob[h].cardinality = M; ob[h].score = score;
+        ob[h].precision = precision_of(score, cfg.input_mu);
+        bins[bidx[h]] = ob[h];
+        bup[bidx[h]] = upper;
+        bprec[bidx[h]] = (signed char)ob[h].precision;
+    }
+    __syncwarp();
+    // ---- LUTs over [kmin, kmax] (lane's keys): bin id, pass-2 descriptor
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        const int k = kmin + j;
+        if (k > kmax) continue;
+        const bool present = (P >> j) & 1ull;
+        const int b = present ? __popcll(S & ((2ull << j) - 1ull)) - 1 : -1;   // starts <= j, minus 1
+        lut_bin[k] = b;
+        uint32_t d = 0;
+        if (b >= 0) {
+            const int pr = bprec[b];
+            if ((pr == QDOT_HALF || pr == QDOT_SINGLE) && status == QDOT_OK) {
+                const long long delta = bup[b] - (long long)(k - KOFF);
+                if (delta > 0 || A[A_HOT + k] > 0) {
+                    d = P2_NEED | (pr == QDOT_HALF ? P2_HALF : 0u) | (uint32_t)(delta > P2_DELTA_MAX ? P2_DELTA_MAX : delta);
+                    need = 1;
+                    if (A[A_PRIV + k] > 0) priv = 1;
+                }
+            }
+        }
+        lut_p2[k] = d;
+    }
+    need = __reduce_or_sync(0xffffffffu, need);
+    priv = __reduce_or_sync(0xffffffffu, priv);
+    if (need) need = (!priv && a_listovf == 0) ? 2 : 1;
+    ScoreMeta m;
+    m.status = status; m.n_bins = nb; m.e_min = e_min; m.e_max = e_max;
+    m.early = early; m.need_p2 = need; m.degenerate = 0; m.input_mu = cfg.input_mu;
+    m.done = need ? 0 : 1; m.pad_ = 0;
+    m.nnz = (long long)nnz; m.zero = a_zero; m.n_total = n_total; m.eps_eff = eps_eff;
+    if (lane == 0) *meta = m;
+    unsigned long long ts1 = 0;
+    if (lane == 0) { ts1 = global_ns(); ws_stamps(A)[1] = ts1; }
+    if (need) return;                                                    // pass 2 finalizes
+    __syncwarp();
+    // ---- bin values, precision counts, fold, header
+    long long cnt_local[4] = {0, 0, 0, 0};
+    int ovf = 0, half = 0;
+    const GlobalKeys kk{A, B, lut_p2};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        if (bidx[h] < 0 || status != QDOT_OK) continue;
+        int o = 0, hf = 0;
+        const double v = bin_value(kk, ob[h], &o, &hf);
+        ovf |= o;
+        half |= hf;
+        bins[bidx[h]].value = v;
+        bins[bidx[h]].flags = hf;
+        sval[bidx[h]] = v;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) cnt_local[p] += ob[h].precision == p ? ob[h].cardinality : 0;
+    }
+    ovf = __reduce_or_sync(0xffffffffu, ovf);
+    half = __reduce_or_sync(0xffffffffu, half);
+    unsigned long long s_cnt[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        long long v = cnt_local[p];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        s_cnt[p] = (unsigned long long)v;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        double sum = 0.0, cc = 0.0;
+        neumaier_fold(sval, status == QDOT_OK ? nb : 0, sum, cc);
+        write_result(ts0, ts1, m, sum, cc, s_cnt, ovf, half, res);
+    }
+}
 // =============================================================================
 // score (one CTA)
 // =============================================================================
@@ -425,6 +644,20 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
         kmin = (int)(r >> 16);
         kmax = KEYS - (int)(r & 0xFFFFu);
     }
+    // one device, keys spanning < 64 exponents: one warp scores (and finalizes)
+#ifndef QDOT_NO_SCORE_WARP
+    if (fuse && kmax >= kmin && kmax - kmin < SW_KEYS) {
+        if (tid < 32) {
+            const long long nf0 = __shfl_sync(0xffffffffu, a_nonfinite, 0);
+            const long long z0 = __shfl_sync(0xffffffffu, a_zero, 0);
+            const long long lo0 = __shfl_sync(0xffffffffu, a_listovf, 0);
+            const unsigned long long t0 = __shfl_sync(0xffffffffu, ts0, 0);
+            score_warp(A, B, lut_bin, lut_p2, meta, res, bins, n_total, cfg, kmin, kmax, t0, nf0, z0, lo0, S.sval,
+                       S.bup, S.bprec);
+        }
+        return;
+    }
+#endif
     // cached path: stage the key rows the bin values and the LUT read
     const bool kcache = fuse && kmax >= kmin && kmax - kmin < KC_SPAN;
     for (int j = tid; kcache && j <= kmax - kmin; j += SC_T) {
