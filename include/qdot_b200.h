@@ -320,6 +320,12 @@ int qdot_b200_read_probe(const double* x, int64_t n, double* out, void* stream);
 /* --- host-side helpers (no GPU needed; exported for tests and bindings) ----- */
 /* correctly rounded acc * 2^u with math.ldexp semantics; *overflow set on range error */
 double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow);
+/* the report's bound sums over a fetched bin table (scoring.py:171-199,
+ * kernel.py:205-222): out[0] = math.fsum of M * ldexp(eps(precision),
+ * upper - shift + 1) over the bins, out[1] = their left-to-right sum from 0.0.
+ * shift = 0: abs_bound; e_max: rel_bound; reference.flexp_e: rel_bound_e.
+ * QDOT_ERR_OVERFLOW where the reference raises OverflowError. */
+int qdot_b200_bound_sums(const qdot_bin* bins, int32_t n_bins, int64_t shift, double* out);
 
 #ifdef __cplusplus
 }

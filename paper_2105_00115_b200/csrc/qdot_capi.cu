@@ -460,6 +460,48 @@ int qdot_b200_batched_bins(const double* X, const double* Y, int64_t rows, int64
     return QDOT_OK;
 }
 
+// host: the report's error-bound sums over a fetched bin table
+// (scoring.py:171-199, kernel.py:205-222): term_b = M_b * ldexp(eps(p_b),
+// u_b - shift + 1); out[0] = fsum(terms) (correctly rounded: exact big-integer
+// sum, one rounding), out[1] = left-to-right sum from 0.0.  An ldexp that
+// overflows, or an fsum of finite terms that does, is QDOT_ERR_OVERFLOW
+// (the reference raises OverflowError).
+int qdot_b200_bound_sums(const qdot_bin* bins, int32_t n_bins, int64_t shift, double* out) {
+    if (!out || n_bins < 0 || (n_bins > 0 && !bins)) return QDOT_ERR_ARG;
+    static const int kMu[4] = {0, 10, 23, 52};    // PrecisionLevel mantissa bits: eps = 2^-mu
+    BigSum<72> acc;
+    acc.init(-1074, 72);
+    double plain = 0.0;
+    bool inf = false;
+    for (int32_t i = 0; i < n_bins; ++i) {
+        const int p = bins[i].precision;
+        if (p < 0 || p > 3) return QDOT_ERR_ARG;
+        const int64_t k = bins[i].upper - shift + 1 - kMu[p];
+        if (k > 1023) return QDOT_ERR_OVERFLOW;                       // math.ldexp overflow
+        const double pw = k < -1100 ? 0.0 : std::ldexp(1.0, (int)k);   // exact, or rounded below 2^-1074
+        const double t = (double)bins[i].cardinality * pw;
+        plain += t;
+        if (std::isinf(t)) { inf = true; continue; }
+        if (t == 0.0) continue;
+        uint64_t b;
+        std::memcpy(&b, &t, 8);
+        const int e = (int)((b >> 52) & 0x7FF);
+        uint64_t m = b & ((1ull << 52) - 1);
+        int ex = -1074;
+        if (e) { m |= 1ull << 52; ex = e - 1075; }
+        acc.add((__int128)m, ex);                                     // terms are >= 0
+    }
+    if (inf) {
+        out[0] = INFINITY;
+    } else {
+        int ovf = 0;
+        out[0] = acc.round(52, -1022, 1023, &ovf);
+        if (ovf) return QDOT_ERR_OVERFLOW;                            // fsum intermediate overflow
+    }
+    out[1] = plain;
+    return QDOT_OK;
+}
+
 double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow) {
     int o = 0;
     double r = ldexp_rn(acc, u, &o);

@@ -105,8 +105,11 @@ def thread_state(device=None) -> ThreadState:
 
 
 def stream_handle(device) -> int:
+    """The current CUDA stream of `device` (torch's raw getter: the Stream
+    object of torch.cuda.current_stream costs several microseconds per call)."""
     torch = _torch()
-    return int(torch.cuda.current_stream(device).cuda_stream)
+    idx = device.index if getattr(device, "index", None) is not None else torch.cuda.current_device()
+    return int(torch._C._cuda_getCurrentRawStream(idx))
 
 
 def config_struct(cfg, strategy) -> _lib.QdotConfig:

@@ -11,14 +11,14 @@ reference.  Underneath, one call is (csrc/, include/qdot_b200.h):
           -> pass2 (only if a HALF/SINGLE bin has upper != e for a member)
           -> finalize (per-bin values, Neumaier fold) -> fetch (small D2H)
 
-The report's bounds are computed here with math.fsum over the per-bin terms
-exactly as kernel.py:205-222 does.
+The report's bounds are the fsum / left-to-right sums of the per-bin terms of
+kernel.py:205-222, computed by the library's host code over the fetched bin
+table (qdot_b200_bound_sums: exact, rounded once -- math.fsum's result).
 """
 
 from __future__ import annotations
 
 import ctypes
-import math
 from dataclasses import dataclass, field
 from typing import Dict, Optional
 
@@ -194,7 +194,6 @@ _BIN_DTYPE = np.dtype([("lower", "<i8"), ("upper", "<i8"), ("cardinality", "<i8"
                        ("precision", "<i4"), ("first_key", "<i4"), ("last_key", "<i4"), ("flags", "<i4"),
                        ("value", "<f8")])
 assert _BIN_DTYPE.itemsize == ctypes.sizeof(_lib.QdotBin)
-_EPS_OF_CODE = np.array([PrecisionLevel.from_code(c).eps for c in range(4)])
 
 
 def _bin_rows(cbins, n_bins: int) -> np.ndarray:
@@ -205,33 +204,18 @@ def _bin_rows(cbins, n_bins: int) -> np.ndarray:
     return np.frombuffer(cbins, dtype=_BIN_DTYPE, count=n_bins).copy()
 
 
-_EPS_LIST = [float(e) for e in _EPS_OF_CODE]
-_SMALL_TABLE = 256          # bin tables up to this size: scalar math (numpy's per-call cost dominates)
-
-
-def _bound_terms(rows: np.ndarray, shift: int):
-    """M * ldexp(eps, upper - shift + 1) per bin, rounded exactly like the
-    scalar terms of scoring.py:171-178 (ldexp first, then the product).  An
-    overflowing ldexp raises OverflowError like the reference's math.ldexp.
-    Returns a list of floats."""
-    if rows.size <= _SMALL_TABLE:
-        return [float(c) * math.ldexp(_EPS_LIST[p], u - shift + 1)
-                for c, p, u in zip(rows["cardinality"].tolist(), rows["precision"].tolist(), rows["upper"].tolist())]
-    eps = _EPS_OF_CODE[rows["precision"]]
-    k = rows["upper"] - shift + 1
-    with np.errstate(over="ignore"):
-        p2 = np.ldexp(eps, np.clip(k, -4000, 4000))
-    if not np.all(np.isfinite(p2)):
-        p2 = np.array([math.ldexp(float(e), int(kk)) for e, kk in zip(eps, k)])
-    return (rows["cardinality"].astype(np.float64) * p2).tolist()
-
-
-def _plain_sum(terms) -> float:
-    """Left-to-right sum from 0.0 (scoring.py:195-199)."""
-    acc = 0.0
-    for t in terms:
-        acc += t
-    return acc
+def _bound_sums(cbins, n_bins: int, shift: int):
+    """(fsum, left-to-right sum) of M * ldexp(eps(precision), upper - shift + 1)
+    over the fetched bin table (scoring.py:171-199, kernel.py:205-222), in the
+    library's host code (qdot_b200_bound_sums: exact big-integer sum rounded
+    once, i.e. math.fsum).  OverflowError where math.ldexp / fsum raise it."""
+    lib = _lib.load()
+    out = (ctypes.c_double * 2)()
+    rc = lib.qdot_b200_bound_sums(cbins, int(n_bins), int(shift), out)
+    if rc == _lib.QDOT_ERR_OVERFLOW:
+        raise OverflowError("math range error")
+    _lib.check(rc, lib)
+    return out[0], out[1]
 
 
 def _make_bin_objects(rows: np.ndarray, indexer):
@@ -250,10 +234,9 @@ def _build_params(res, cbins, cfg, strategy, indexer, rows=None) -> ParameterSet
                       early_terminated=bool(res.early_terminated), n=int(res.n), eps_eff=float(res.eps_eff),
                       n_bins=int(res.n_bins), zero_count=int(res.zero_count), _indexer=indexer,
                       _make_bins=_make_bin_objects(rows, indexer))
-    # ParameterSet.rel_bound: plain left-to-right sum from 0.0 (scoring.py:195-199)
-    rel = _bound_terms(rows, int(res.e_max))
-    ps.rel_bound = _plain_sum(rel)
-    ps._rel_terms = rel
+    # ParameterSet.rel_bound: plain left-to-right sum from 0.0 (scoring.py:195-199);
+    # the report's rel_bound: fsum of the same terms (kernel.py:213)
+    ps._rel_fsum, ps.rel_bound = _bound_sums(cbins, int(res.n_bins), int(res.e_max))
     return ps
 
 
@@ -301,8 +284,8 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
     """Host-side report assembly (kernel.py:205-240)."""
     rows = _bin_rows(cbins, int(res.n_bins))
     params = _build_params(res, cbins, cfg, strategy, indexer, rows)
-    abs_bound = math.fsum(_bound_terms(rows, 0))
-    rel_bound = math.fsum(params._rel_terms)
+    abs_bound = _bound_sums(cbins, int(res.n_bins), 0)[0]
+    rel_bound = params._rel_fsum
     rel_hypothesis = "assumed"
     rel_bound_e = None
     if is_norm:
@@ -314,7 +297,7 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
         else:
             holds = params.e_max <= fe or rows.size == 0
             rel_hypothesis = "holds" if (holds or is_norm) else "violated"
-            rel_bound_e = math.fsum(_bound_terms(rows, int(fe)))
+            rel_bound_e = _bound_sums(cbins, int(res.n_bins), int(fe))[0]
     counts = {level: 0 for level in PrecisionLevel}
     for i, level in enumerate((PrecisionLevel.PERFORATE, PrecisionLevel.HALF, PrecisionLevel.SINGLE,
                                PrecisionLevel.DOUBLE)):

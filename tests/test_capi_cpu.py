@@ -172,3 +172,48 @@ def test_enums_interoperate_with_reference_style_enums():
     cfg = Q.ToleranceConfig(1e-3, split=RefSplit.PER_BIN)
     from paper_2105_00115_b200.device import config_struct
     assert config_struct(cfg, None).split == 1
+
+
+def test_bound_sums_match_fsum():
+    """qdot_b200_bound_sums (host code, no GPU) equals math.fsum and the plain
+    left-to-right sum of the reference's bound terms (scoring.py:171-199),
+    including ldexp underflow, and raises where math.ldexp overflows."""
+    import ctypes
+    import math
+    import random
+
+    from paper_2105_00115_b200 import _lib
+    lib = _lib.load(build_if_missing=False)
+    mus = [0, 10, 23, 52]
+    out = (ctypes.c_double * 2)()
+    rnd = random.Random(7)
+    for trial in range(1500):
+        nb = rnd.randint(0, 50)
+        arr = (_lib.QdotBin * max(nb, 1))()
+        shift = rnd.randint(-60, 60)
+        terms = []
+        for i in range(nb):
+            b = arr[i]
+            b.cardinality = rnd.choice([1, 2, 3, rnd.randint(1, 1 << 40)])
+            b.precision = rnd.randint(0, 3)
+            b.upper = rnd.randint(-1200, 1000) if trial % 3 == 0 else rnd.randint(-60, 60)
+            try:
+                terms.append(float(b.cardinality) * math.ldexp(math.ldexp(1.0, -mus[b.precision]),
+                                                               b.upper - shift + 1))
+            except OverflowError:
+                terms = None
+                break
+        rc = lib.qdot_b200_bound_sums(arr, nb, shift, out)
+        if terms is None:
+            assert rc == _lib.QDOT_ERR_OVERFLOW
+            continue
+        plain = 0.0
+        for t in terms:
+            plain += t
+        try:
+            f = math.fsum(terms)
+        except OverflowError:
+            assert rc == _lib.QDOT_ERR_OVERFLOW
+            continue
+        assert rc == 0
+        assert out[0] == f and out[1] == plain, (trial, out[0], f, out[1], plain)
