@@ -263,11 +263,12 @@ def time_reference(n_sample: int, steps: int, warm: int):
         t0 = time.perf_counter()
         R.qdot(x, y, cfg)
         times.append(time.perf_counter() - t0)
-    best = min(times)
-    return {"value": n_sample / best, "unit": "elements/s", "cores": 1, "kind": "reference",
+    mean = sum(times) / len(times)
+    return {"value": n_sample / mean, "unit": "elements/s", "cores": 1, "kind": "reference",
             "sample": f"reference qdot 0.1.0 (baseline/_ref, unmodified) on n={n_sample} standard-normal "
-                      f"x, y (default_rng(0)), eps=1e-8, exact; best of {len(times)} after {warm} warm-up",
-            "ms_per_call": best * 1e3, "host_cores_available": os.cpu_count()}
+                      f"x, y (default_rng(0)), eps=1e-8, exact; mean of {len(times)} timed calls after "
+                      f"{warm} warm-up",
+            "ms_per_call": mean * 1e3, "ms_best": min(times) * 1e3, "host_cores_available": os.cpu_count()}
 
 
 def time_port(n_sample: int, steps: int = 2):
@@ -432,8 +433,10 @@ def measure_secondary(lib, _lib, torch, dev, stream, xd, yd, n, norm, Q, config_
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 3))
-    warm = min(max(args.warmup, 0), 1)
+    # the requested K / W (each step ~0.9 s on the 2^24 sample), capped so the
+    # arm stays within about a minute and a half
+    steps = max(1, min(args.steps, 60))
+    warm = min(max(args.warmup, 0), 10)
     ref = time_reference(args.ref_sample, steps, warm)
     port = time_port(args.cpu_sample, steps)
     base = ref if ref is not None else port

@@ -514,3 +514,27 @@ def test_inputs_written_just_before_the_call_are_seen(n):
     for i in range(2):
         x.copy_(xsrc[i])
         assert agree(Q.qdot(x, x, cfg), O.qdot(xs[i], xs[i], 1e-8)), i
+
+
+@pytest.mark.parametrize("n", [606_209, (1 << 21) + 777, 1 << 22])
+@pytest.mark.parametrize("data", ["normal", "wide", "special"])
+def test_norm_ring_pass1_against_oracle(n, data, pass1_mode):
+    """Norm mode above the compact pass-1 size (the streaming k_pass1): bins and
+    value bit-exact against the oracle in every pass-1 mode, with a partial
+    last tile (odd n), zeros, subnormals and wide exponents."""
+    rng = np.random.default_rng(n % 1000 + len(data))
+    x = rng.standard_normal(n)
+    if data == "wide":
+        x *= np.exp2(rng.integers(-300, 300, n))
+    elif data == "special":
+        x[rng.integers(0, n, 500)] = 0.0
+        x[rng.integers(0, n, 50)] = 5e-320
+        x[rng.integers(0, n, 50)] *= 2.0 ** 500
+    eps = 1e-8 if data != "wide" else 1e-3
+    r = O.qdot(x, x, eps, "none", 52, "exact", members=True)
+    xd = torch.from_numpy(x).cuda()
+    rep = Q.qdot(xd, xd, Q.ToleranceConfig(eps))
+    assert [[b.lower, b.upper, b.cardinality, b.score, b.precision.code] for b in rep.params.bins] == \
+        [[b.lower, b.upper, b.cardinality, b.score, b.precision] for b in r.bins]
+    assert_bins_exact(x, x, rep, r)
+    assert rep.params.zero_count == r.zero_count
