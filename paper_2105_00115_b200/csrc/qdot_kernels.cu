@@ -435,7 +435,7 @@ __device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restr
         early = (long long)(kmax - kmin) <= (-fle - mu_hat);
     }
     // ---- bin starts (bit j: key kmin + j starts a bin)
-    const int jmin = 0, jmax = kmax - kmin;
+    const int jmin = 0;
     unsigned long long S;
     const int strategy = cfg.strategy;
     if (early) {
