@@ -317,6 +317,32 @@ int qdot_b200_generate(int law, double param, uint64_t seed, int64_t offset, int
  * discard them: the HBM read ceiling bench.py reports next to the copy peak */
 int qdot_b200_read_probe(const double* x, int64_t n, double* out, void* stream);
 
+/* --- device-resident solver loop (apps.py:178-229 without a host round trip
+ * per iteration): a CUDA graph whose single WHILE-conditional node runs a body
+ * the caller captures on `stream` between _loop_create and _loop_finish (the
+ * iteration's SpMV, qdot pipelines, scalar recurrence and vector updates),
+ * ending with qdot_b200_acg_check: it records iteration k (both dots' result
+ * headers and the scalar state st[0..7], 576 bytes) into rec[k] and clears
+ * the condition once the host loop would stop (a dot's status, p.Ap not finite
+ * or <= 0, r.r < 0, sqrt(r.r) <= tau = st[7], or k + 1 == cap).  counter =
+ * {k, cap} (device int64[2]) is set by the caller before each launch. */
+int qdot_b200_loop_create(void* stream, void** loop, unsigned long long* handle);
+int qdot_b200_loop_finish(void* loop, void* stream);
+int qdot_b200_loop_launch(void* loop, void* stream);
+void qdot_b200_loop_destroy(void* loop);
+int qdot_b200_acg_check(const void* ws_a, const void* ws_b, const double* st, void* rec, long long* counter,
+                        unsigned long long handle, void* stream);
+/* fused ACG iteration tail for the loop body (apps.py:212-223): cg_xr computes
+ * alpha = st[0] / d (d = the p.Ap result in ws_pq), x += alpha p, r -= alpha q
+ * (products rounded first, as numpy); cg_p_check computes beta = c_new / st[0]
+ * (c_new = the r.r result in ws_rr), p = r + beta p, and then, in the last
+ * CTA, advances st (c, beta, sqrt(c)) and does qdot_b200_acg_check's record and
+ * condition.  counter = {k, cap, ticket} (device int64[3], ticket 0). */
+int qdot_b200_cg_xr(int64_t n, const void* ws_pq, double* st, double* x, const double* p, double* r,
+                    const double* q, void* stream);
+int qdot_b200_cg_p_check(int64_t n, const void* ws_pq, const void* ws_rr, double* st, const double* r, double* p,
+                         void* rec, long long* counter, unsigned long long handle, void* stream);
+
 /* --- host-side helpers (no GPU needed; exported for tests and bindings) ----- */
 /* correctly rounded acc * 2^u with math.ldexp semantics; *overflow set on range error */
 double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow);

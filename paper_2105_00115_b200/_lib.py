@@ -92,6 +92,13 @@ SIGNATURES = {
     "qdot_b200_vec_update_dev": (_I, [_I64, _I, _P, _P, _P, _P, _P]),
     "qdot_b200_solver_scalar": (_I, [_I, _P, _P, _P]),
     "qdot_b200_publish_iter": (_I, [_P, _P, _P, _P, _P, _P]),
+    "qdot_b200_loop_create": (_I, [_P, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_ulonglong)]),
+    "qdot_b200_loop_finish": (_I, [_P, _P]),
+    "qdot_b200_loop_launch": (_I, [_P, _P]),
+    "qdot_b200_loop_destroy": (None, [_P]),
+    "qdot_b200_acg_check": (_I, [_P, _P, _P, _P, _P, ctypes.c_ulonglong, _P]),
+    "qdot_b200_cg_xr": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P]),
+    "qdot_b200_cg_p_check": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_ulonglong, _P]),
     "qdot_b200_exact_workspace_bytes": (ctypes.c_size_t, []),
     "qdot_b200_exact_region_words": (_I64, []),
     "qdot_b200_exact_begin": (_I, [_P, _P]),

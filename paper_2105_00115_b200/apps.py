@@ -416,6 +416,75 @@ class _IterGraph:
         _lib.check(self.lib.qdot_b200_solver_scalar(which, self.ws[k].data_ptr(), self.st.data_ptr(), stream),
                    self.lib)
 
+    # ---- device-resident loop (ACG): a WHILE-conditional graph whose body is
+    # one iteration ending with qdot_b200_acg_check (records the iteration,
+    # sets the loop condition); one launch and one host wake-up per solve
+    LOOP_CAP = 4096                                           # iterations per launch (record buffer)
+
+    def check(self, handle: int, stream: int) -> None:
+        _lib.check(self.lib.qdot_b200_acg_check(self.ws[0].data_ptr(), self.ws[1].data_ptr(), self.st.data_ptr(),
+                                                self.rec.data_ptr(), self.ctr.data_ptr(), handle, stream),
+                   self.lib)
+
+    def cg_xr(self, x, p, r, q, stream: int) -> None:
+        _lib.check(self.lib.qdot_b200_cg_xr(x.shape[0], self.ws[0].data_ptr(), self.st.data_ptr(), x.data_ptr(),
+                                            p.data_ptr(), r.data_ptr(), q.data_ptr(), stream), self.lib)
+
+    def cg_p_check(self, r, p, handle: int, stream: int) -> None:
+        _lib.check(self.lib.qdot_b200_cg_p_check(r.shape[0], self.ws[0].data_ptr(), self.ws[1].data_ptr(),
+                                                 self.st.data_ptr(), r.data_ptr(), p.data_ptr(), self.rec.data_ptr(),
+                                                 self.ctr.data_ptr(), handle, stream), self.lib)
+
+    def capture_loop(self, body):
+        """Build the loop graph: `body(stream, handle)` is captured as the
+        WHILE node's body on a side stream (nothing runs yet)."""
+        torch, device = _dev()
+        self.ctr = torch.zeros(3, dtype=torch.int64, device=self.st.device)    # k, cap, CTA ticket
+        self.ctr_host = torch.zeros(3, dtype=torch.int64).pin_memory()
+        self.rec = torch.empty(self.LOOP_CAP * 576, dtype=torch.uint8, device=self.st.device)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        loop = ctypes.c_void_p()
+        handle = ctypes.c_ulonglong()
+        _lib.check(self.lib.qdot_b200_loop_create(side.cuda_stream, ctypes.byref(loop), ctypes.byref(handle)),
+                   self.lib)
+        self.loop = loop
+        try:
+            with torch.cuda.stream(side):
+                body(side.cuda_stream, handle.value)
+        finally:
+            _lib.check(self.lib.qdot_b200_loop_finish(loop, side.cuda_stream), self.lib)
+        torch.cuda.current_stream().wait_stream(side)
+
+    def run_loop(self, cap: int, tau: float):
+        """Run up to `cap` iterations on the device (st[0] = c set by the
+        caller); returns [(result header of ws 0, of ws 1, st)] per iteration."""
+        torch, _ = _dev()
+        stream = torch.cuda.current_stream()
+        self.st[7] = tau
+        self.ctr_host[0] = 0
+        self.ctr_host[1] = cap
+        self.ctr_host[2] = 0
+        self.ctr.copy_(self.ctr_host, non_blocking=True)
+        _lib.check(self.lib.qdot_b200_loop_launch(self.loop, stream.cuda_stream), self.lib)
+        k = int(self.ctr[0].item())                       # waits for the loop
+        buf = self.rec[:k * 576].cpu().numpy().tobytes()
+        out = []
+        for i in range(k):
+            b = buf[i * 576:(i + 1) * 576]
+            out.append((_lib.QdotResult.from_buffer_copy(b[0:ctypes.sizeof(_lib.QdotResult)]),
+                        _lib.QdotResult.from_buffer_copy(b[256:256 + ctypes.sizeof(_lib.QdotResult)]),
+                        np.frombuffer(b[512:576], dtype=np.float64)))
+        return out
+
+    def __del__(self):
+        loop = getattr(self, "loop", None)
+        if loop is not None and loop.value:
+            try:
+                self.lib.qdot_b200_loop_destroy(loop)
+            except Exception:
+                pass
+
     def publish(self, stream: int) -> None:
         _lib.check(self.lib.qdot_b200_publish_iter(self.ws[0].data_ptr(), self.ws[1].data_ptr(), self.st.data_ptr(),
                                                    self.host_t.data_ptr(), self.seq_dev.data_ptr(), stream),
@@ -524,43 +593,43 @@ def _acg(a, b, x0, tau, max_iters, cfg, strategy, torch, device, n, use_graph, e
 
     k = 0
     if use_graph and resid > tau:
-        # one CUDA graph per iteration: SpMV, p.Ap, alpha, x and r updates, r.r,
-        # beta, p update, publish -- one host wake-up per iteration
+        # the iterations run on the device: one CUDA graph whose WHILE node
+        # repeats SpMV, p.Ap, alpha, x and r updates, r.r, beta, p update and
+        # the check node (records the iteration, decides whether to go on);
+        # one launch and one host wake-up per solve (or per LOOP_CAP iterations)
         if cached:
-            G, g = entry.G, entry.graphs
+            G = entry.G
         else:
             G = _IterGraph(device)
             cst = config_struct(cfg, strategy)
 
-            def body(stream):
+            def body(stream, handle):
                 a.matvec_device(p, out=q)
                 G.qdot_nodes(0, p, q, False, cst, stream)
-                G.scalar(0, 0, stream)                          # alpha = c / d
-                G.update(_ADD, x, 1, p, x, stream)              # x = x + alpha * p
-                G.update(_SUB, r, 1, q, r, stream)              # r = r - alpha * q
+                G.cg_xr(x, p, r, q, stream)                     # alpha = c / d; x += alpha p; r -= alpha q
                 G.qdot_nodes(1, r, r, True, cst, stream)
-                G.scalar(1, 1, stream)                          # beta = c_new / c; c = c_new
-                G.update(_ADD, r, 2, p, p, stream)              # p = r + beta * p
-                G.publish(stream)
+                G.cg_p_check(r, p, handle, stream)              # beta = c_new / c; p = r + beta p; c = c_new; check
 
-            g = G.capture(body)
+            a.device_arrays()                                   # host->device copies cannot be captured
+            a.sell_arrays()
+            G.capture_loop(body)
             if entry is not None:
-                entry.G, entry.graphs, entry.bufs = G, g, (x, r, p, q)
+                entry.G, entry.graphs, entry.bufs = G, None, (x, r, p, q)
         G.st[0] = c
         while resid > tau and k < max_iters:
-            r_pq, r_rr, st = G.run(g)
-            d_rep = _dot_report(r_pq)
-            d = d_rep.value
-            if not math.isfinite(d) or d <= 0.0:
-                raise BreakdownError(f"p.Ap = {d!r} at iteration {k}")
-            c_rep = _dot_report(r_rr)
-            if not (c_rep.value >= 0.0):                      # apps.py:171-175
-                raise AssertionError("norm computed by qdot must be nonnegative")
-            c = c_rep.value
-            resid = math.sqrt(c)
-            k += 1
-            trace.record(k, "pAp", d_rep, resid)
-            trace.record(k, "rtr", c_rep, resid)
+            for r_pq, r_rr, st in G.run_loop(min(max_iters - k, G.LOOP_CAP), tau):
+                d_rep = _dot_report(r_pq)
+                d = d_rep.value
+                if not math.isfinite(d) or d <= 0.0:
+                    raise BreakdownError(f"p.Ap = {d!r} at iteration {k}")
+                c_rep = _dot_report(r_rr)
+                if not (c_rep.value >= 0.0):                  # apps.py:171-175
+                    raise AssertionError("norm computed by qdot must be nonnegative")
+                c = c_rep.value
+                resid = math.sqrt(c)
+                k += 1
+                trace.record(k, "pAp", d_rep, resid)
+                trace.record(k, "rtr", c_rep, resid)
     while resid > tau and k < max_iters:
         a.matvec_device(p, out=q)
         d_rep = dots(p, q, False)

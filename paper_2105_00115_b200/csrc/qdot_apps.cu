@@ -166,9 +166,189 @@ __global__ void k_publish_iter(const void* ws_a, const void* ws_b, const double*
     }
 }
 
+// ---- device-resident solver loop: the check node of a WHILE-conditional graph
+// body.  Records iteration k (the two result headers and st, the block
+// k_publish_iter publishes) into rec[k] and keeps looping while the host
+// loop of apps.py:178-229 would: both dots OK, p.Ap finite and > 0, r.r >= 0,
+// sqrt(r.r) > tau (IEEE sqrt = math.sqrt), k + 1 < cap.  counter = {k, cap}
+// and tau = st[7] are set by the host before each launch (the graph is reused
+// across solves and chunks).
+constexpr int REC_BYTES = 576;
+__global__ void k_acg_check(const void* ws_a, const void* ws_b, const double* st, unsigned char* rec,
+                            long long* counter, cudaGraphConditionalHandle handle) {
+    const int t = threadIdx.x;
+    const long long k = counter[0], cap = counter[1];
+    const double tau = st[7];
+    const uint32_t* ra = reinterpret_cast<const uint32_t*>(static_cast<const char*>(ws_a) + qd::OFF_RESULT);
+    const uint32_t* rb = reinterpret_cast<const uint32_t*>(static_cast<const char*>(ws_b) + qd::OFF_RESULT);
+    uint32_t* h = reinterpret_cast<uint32_t*>(rec + k * REC_BYTES);
+    if (t < 64) h[t] = ra[t];
+    else if (t < 128) h[t] = rb[t - 64];
+    else if (t < 144) h[t] = reinterpret_cast<const uint32_t*>(st)[t - 128];
+    if (t == 0) {
+        const qdot_result* r0 = reinterpret_cast<const qdot_result*>(ra);
+        const qdot_result* r1 = reinterpret_cast<const qdot_result*>(rb);
+        const double d = r0->value, c = r1->value;
+        const bool go = r0->status == QDOT_OK && r1->status == QDOT_OK && (d - d == 0.0) && d > 0.0 && c >= 0.0 &&
+                        __dsqrt_rn(c) > tau && k + 1 < cap;
+        *counter = k + 1;
+        cudaGraphSetConditional(handle, go ? 1u : 0u);
+    }
+}
+
+// ---- fused ACG iteration kernels for the device loop (apps.py:212-223):
+// x = x + alpha p and r = r - alpha q with alpha = c / d computed per thread
+// (c = st[0], d = the p.Ap dot in ws_pq); the products rounded first like the
+// numpy expressions.  Block 0 records alpha and d in st.
+__global__ void __launch_bounds__(T) k_cg_xr(int64_t n, const void* ws_pq, double* st, double* x,
+                                             const double* __restrict__ p, double* r, const double* __restrict__ q) {
+    const double d = result_value(ws_pq);
+    const double alpha = __ddiv_rn(st[0], d);
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += (int64_t)gridDim.x * T) {
+        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+        r[i] = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st[1] = alpha; st[4] = d; }
+}
+
+// p = r + beta p with beta = c_new / c (c_new = the r.r dot in ws_rr); the last
+// CTA to finish (ticket counter[2]) then runs the check of k_acg_check and
+// advances the recurrence: st[0] = c_new, st[2] = beta, st[3] = sqrt(c_new).
+__global__ void __launch_bounds__(T) k_cg_p_check(int64_t n, const void* ws_pq, const void* ws_rr, double* st,
+                                                  const double* __restrict__ r, double* p, unsigned char* rec,
+                                                  long long* counter, cudaGraphConditionalHandle handle) {
+    const double c_new = result_value(ws_rr);
+    const double beta = __ddiv_rn(c_new, st[0]);
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += (int64_t)gridDim.x * T)
+        p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+    __threadfence();
+    __syncthreads();
+    __shared__ int last;
+    if (threadIdx.x == 0)
+        last = atomicAdd(reinterpret_cast<unsigned long long*>(counter + 2), 1ull) == (unsigned long long)gridDim.x - 1ull;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int t = threadIdx.x;
+    const long long k = counter[0], cap = counter[1];
+    const qdot_result* r0 = reinterpret_cast<const qdot_result*>(static_cast<const char*>(ws_pq) + qd::OFF_RESULT);
+    const qdot_result* r1 = reinterpret_cast<const qdot_result*>(static_cast<const char*>(ws_rr) + qd::OFF_RESULT);
+    __shared__ bool go;
+    if (t == 0) {
+        const double d = r0->value;
+        const double sq = __dsqrt_rn(c_new);
+        go = r0->status == QDOT_OK && r1->status == QDOT_OK && (d - d == 0.0) && d > 0.0 && c_new >= 0.0 &&
+             sq > st[7] && k + 1 < cap;
+        st[0] = c_new;
+        st[2] = beta;
+        st[3] = sq;
+    }
+    __syncthreads();
+    const uint32_t* ra = reinterpret_cast<const uint32_t*>(r0);
+    const uint32_t* rb = reinterpret_cast<const uint32_t*>(r1);
+    uint32_t* h = reinterpret_cast<uint32_t*>(rec + k * REC_BYTES);
+    if (t < 64) h[t] = ra[t];
+    else if (t < 128) h[t] = rb[t - 64];
+    else if (t < 144) h[t] = reinterpret_cast<const uint32_t*>(st)[t - 128];
+    if (t == 0) {
+        counter[0] = k + 1;
+        counter[2] = 0;
+        cudaGraphSetConditional(handle, go ? 1u : 0u);
+    }
+}
+
+struct SolverLoop {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphConditionalHandle handle = 0;
+};
+
 }  // namespace
 
 extern "C" {
+
+// A graph with one WHILE node (condition initially 1); the caller's stream
+// then captures the loop body into it until qdot_b200_loop_finish.
+int qdot_b200_loop_create(void* stream, void** loop, unsigned long long* handle) {
+    if (!loop || !handle) return QDOT_ERR_ARG;
+    SolverLoop* L = new SolverLoop();
+    cudaError_t e = cudaGraphCreate(&L->graph, 0);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&L->handle, L->graph, 1u, cudaGraphCondAssignDefault);
+    cudaGraph_t body = nullptr;
+    if (e == cudaSuccess) {
+        cudaGraphNodeParams p = {};
+        p.type = cudaGraphNodeTypeConditional;
+        p.conditional.handle = L->handle;
+        p.conditional.type = cudaGraphCondTypeWhile;
+        p.conditional.size = 1;
+        cudaGraphNode_t node;
+        e = cudaGraphAddNode(&node, L->graph, nullptr, 0, &p);
+        body = p.conditional.phGraph_out ? p.conditional.phGraph_out[0] : nullptr;
+    }
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(static_cast<cudaStream_t>(stream), body, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        if (L->graph) cudaGraphDestroy(L->graph);
+        delete L;
+        return qd::report_cuda_error(e, "loop_create");
+    }
+    *loop = L;
+    *handle = (unsigned long long)L->handle;
+    return QDOT_OK;
+}
+
+int qdot_b200_loop_finish(void* loop, void* stream) {
+    if (!loop) return QDOT_ERR_ARG;
+    SolverLoop* L = static_cast<SolverLoop*>(loop);
+    cudaGraph_t body = nullptr;
+    cudaError_t e = cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &body);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&L->exec, L->graph, 0);
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "loop_finish");
+}
+
+int qdot_b200_loop_launch(void* loop, void* stream) {
+    if (!loop || !static_cast<SolverLoop*>(loop)->exec) return QDOT_ERR_ARG;
+    cudaError_t e = cudaGraphLaunch(static_cast<SolverLoop*>(loop)->exec, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "loop_launch");
+}
+
+void qdot_b200_loop_destroy(void* loop) {
+    if (!loop) return;
+    SolverLoop* L = static_cast<SolverLoop*>(loop);
+    if (L->exec) cudaGraphExecDestroy(L->exec);
+    if (L->graph) cudaGraphDestroy(L->graph);
+    delete L;
+}
+
+int qdot_b200_cg_xr(int64_t n, const void* ws_pq, double* st, double* x, const double* p, double* r,
+                    const double* q, void* stream) {
+    if (n < 0 || !ws_pq || !st || (n > 0 && (!x || !p || !r || !q))) return QDOT_ERR_ARG;
+    const int g = grid_for(n > 0 ? n : 1, 4);
+    k_cg_xr<<<g, T, 0, static_cast<cudaStream_t>(stream)>>>(n, ws_pq, st, x, p, r, q);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "cg_xr");
+}
+
+int qdot_b200_cg_p_check(int64_t n, const void* ws_pq, const void* ws_rr, double* st, const double* r, double* p,
+                         void* rec, long long* counter, unsigned long long handle, void* stream) {
+    if (n < 0 || !ws_pq || !ws_rr || !st || !rec || !counter || (n > 0 && (!r || !p))) return QDOT_ERR_ARG;
+    const int g = grid_for(n > 0 ? n : 1, 4);
+    k_cg_p_check<<<g, T, 0, static_cast<cudaStream_t>(stream)>>>(n, ws_pq, ws_rr, st, r, p,
+                                                                  static_cast<unsigned char*>(rec), counter,
+                                                                  (cudaGraphConditionalHandle)handle);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "cg_p_check");
+}
+
+int qdot_b200_acg_check(const void* ws_a, const void* ws_b, const double* st, void* rec, long long* counter,
+                        unsigned long long handle, void* stream) {
+    if (!ws_a || !ws_b || !st || !rec || !counter) return QDOT_ERR_ARG;
+    k_acg_check<<<1, 160, 0, static_cast<cudaStream_t>(stream)>>>(ws_a, ws_b, st, static_cast<unsigned char*>(rec),
+                                                                   counter, (cudaGraphConditionalHandle)handle);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "acg_check");
+}
 
 int qdot_b200_vec_update_dev(int64_t n, int op, const double* a, const double* s_dev, const double* b, double* out,
                              void* stream) {

@@ -1,0 +1,20 @@
+#!/bin/bash
+# Round-2 evidence: bench (K=20 burst + sustained + e2e), launch list and ncu --set full of the
+# headline step, batched strategies, small-n latency, solver timings, C5 scale, sanitizer on smoke.
+TAG=${1:-r2}
+mkdir -p gpurun_out
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_$TAG.csv \
+   python bench.py --steps 10 --warmup 3 --e2e-steps 0 --no-cpu-baseline --no-secondary --sustained-ms 0 > gpurun_out/ncu_launch_$TAG.log 2>&1
+python tools/ncu_summary.py --launches gpurun_out/launches_$TAG.csv gpurun_out/launches_$TAG > /dev/null 2>&1
+bash scripts/gpu_ncu_one.sh pass1_$TAG k_pass1 python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --no-secondary --sustained-ms 0 > /dev/null 2>&1
+bash scripts/gpu_ncu_one.sh batched_$TAG k_batched python scripts/batched_time.py > /dev/null 2>&1
+timeout 300 python scripts/batched_strategy_time.py > gpurun_out/batched_strat_$TAG.jsonl 2>&1
+timeout 300 python scripts/latency.py > gpurun_out/latency_$TAG.jsonl 2>&1
+( for n in 1000 10000 100000 1000000; do timeout 120 python scripts/step_graph_time.py $n; done ) > gpurun_out/step_graph_$TAG.jsonl 2>&1
+timeout 300 python scripts/solver_bench.py > gpurun_out/solver_bench_$TAG.jsonl 2>&1
+timeout 600 compute-sanitizer --tool memcheck python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/memcheck_smoke_$TAG.log 2>&1
+timeout 600 compute-sanitizer --tool racecheck python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/racecheck_smoke_$TAG.log 2>&1
+cut -c1-300 gpurun_out/bench_$TAG.json; tail -3 gpurun_out/memcheck_smoke_$TAG.log gpurun_out/racecheck_smoke_$TAG.log
+echo done
