@@ -114,6 +114,7 @@ struct P1Params {
     double2* list;           // cold-element list: LIST_SLOTS slots of LIST_PER_SLOT entries,
     uint32_t* list_fill;     // slot b filled by pass-1 CTA b (fill kept across launches)
     int32_t collect;         // fill the list (ranged / split strategies: pass 2 may need it)
+    int32_t per_bin;         // exact strategy with SplitMode.PER_BIN: eps_eff = eps / n_bins
 };
 
 struct ScoreMeta {         // written by the score kernel, read by pass2 / finalize

@@ -57,6 +57,7 @@ struct __align__(16) P1Shared {
     int wide;                                // lean loop over the 24-key window
     int queue;                               // this CTA compacts cold elements through the warp queue
     int kmax;                                // largest sampled key
+    int norm_lean;                           // x . x: exponent-indexed lean loop (window keys base + 2r)
 };
 
 size_t pass1_smem_bytes() { return sizeof(P1Shared); }
@@ -461,6 +462,80 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
     flush();
 }
 
+// ---- norm mode (x . x), lean: every key is 2 ex + KOFF (even), so the P1_W
+// private slots are indexed by the exponent of x (slot r <-> key base + 2r),
+// and a window element needs no exponent sum, no sign and no scale: with
+// m26 = |x| 2^(26 - ex) (x's mantissa bits under the biased exponent 1049),
+// fl(m26 * m26) = fl(x * x) 2^(52 - 2 ex) exactly, so one DMUL and one
+// conversion give the DOUBLE units (emulate.py:133).  Window keys lie in the
+// safe range, so rel < P1_W also excludes zero / subnormal / non-finite x.
+// Returns the tile's cold elements (bit j: xv[j] outside the window).
+template <int V, bool FULLT>
+__device__ __forceinline__ uint32_t p1_tile_norm(char* __restrict__ myb, uint32_t ebase, const double (&xv)[2 * V],
+                                                 int64_t e0, int64_t n, int tid) {
+    uint32_t cold = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * V; ++j) {
+        const uint32_t hi = (uint32_t)__double2hiint(xv[j]);
+        const uint32_t d = (hi & 0x7FF00000u) - ebase;          // (slot of x's exponent) << 20
+        const bool ok = FULLT || e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1) < n;
+        const double m26 = __hiloint2double((int)((hi & 0x000FFFFFu) | 0x41900000u), __double2loint(xv[j]));
+        const long long kd = __double2ll_rn(__dmul_rn(m26, m26));
+        if (d < ((uint32_t)P1_W << 20)) {
+            if (ok) {
+                ulonglong2* slot = reinterpret_cast<ulonglong2*>(myb + (d >> 8));   // slot * P1_T * 16 bytes
+                ulonglong2 v = *slot;
+                v.x += (unsigned long long)kd;
+                v.y += 1ull;
+                *slot = v;
+            }
+        } else if (ok) {
+            cold |= 1u << j;
+        }
+    }
+    return cold;
+}
+
+template <bool VEC, int V, int L2D>
+__device__ __forceinline__ void p1_main_norm(P1Shared& S, const double* __restrict__ x, int64_t n,
+                                             int64_t* __restrict__ A, int64_t* __restrict__ B, int tid,
+                                             uint32_t* zc, uint32_t* nf) {
+    constexpr int EPT = 2 * V;
+    constexpr int TILE = P1_T * EPT;
+    constexpr int FLUSH = 511 / EPT;                   // D < 511 * 2^54 per slot between flushes
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    const int64_t stride = gridDim.x;
+    // slot r holds key base + 2r, i.e. biased exponent fx = r + (base - KOFF) / 2 + 1023
+    const uint32_t ebase = (uint32_t)((S.base - KOFF) / 2 + 1023) << 20;
+    char* __restrict__ myb = reinterpret_cast<char*>(S.priv + tid);
+    const int warp = tid >> 5, lane = tid & 31;
+    int since = 0;
+    uint32_t qn = 0;
+    if (L2D > 0 && tid == 0) {
+        for (int d = 1; d <= L2D; ++d) p1_prefetch_l2<true>(x, x, n, blockIdx.x + d * stride, TILE);
+    }
+    for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
+        double xv[EPT], yv[EPT];
+        bool f;
+        if (L2D > 0 && tid == 0) p1_prefetch_l2<true>(x, x, n, t + (L2D + 1) * stride, TILE);
+        p1_load<true, VEC, V>(x, x, n, t, tid, xv, yv, f);
+        const uint32_t cold = f ? p1_tile_norm<V, true>(myb, ebase, xv, t * TILE, n, tid)
+                                : p1_tile_norm<V, false>(myb, ebase, xv, t * TILE, n, tid);
+        if (__any_sync(0xffffffffu, cold != 0u)) {
+#pragma unroll
+            for (int j = 0; j < EPT; ++j)
+                p1_enqueue(S, A, B, warp, lane, qn, (cold >> j) & 1u, xv[j], xv[j], zc, nf);
+        }
+        if (++since == FLUSH) {
+            p1_drain(S, A, B, warp, lane, qn, zc, nf);
+            p1_flush<false, P1_W>(S, A, B, tid);
+            since = 0;
+        }
+    }
+    p1_drain(S, A, B, warp, lane, qn, zc, nf);
+    p1_flush<false, P1_W>(S, A, B, tid);
+}
+
 // SMALL: the variant for short inputs (a few tiles per CTA), where the fixed
 // per-CTA cost dominates: one main loop (full variants, no queue, no L2
 // prefetch) keeps the code a CTA must fetch small.
@@ -509,6 +584,7 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
             S.full = 1;
             S.wide = 0;
             S.queue = 0;
+            S.norm_lean = 0;
             const bool slot_ok = blockIdx.x < (unsigned)LIST_SLOTS;
             S.list = prm.list + (int64_t)(slot_ok ? blockIdx.x : 0) * LIST_PER_SLOT;
             S.list_fill = slot_ok ? prm.list_fill[blockIdx.x] : (uint32_t)LIST_PER_SLOT;
@@ -659,9 +735,103 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                 const uint32_t ns = pref[KEYS], cov = pref[b + ww] - pref[b];
                 const int qm = (prm.mode >> 2) & 3;
                 S.queue = qm == 1 ? 1 : (qm == 2 ? 0 : ((ns - cov) * 128u > ns));
+                S.norm_lean = 0;
             }
         }
         __syncthreads();
+        if (NORM && (prm.mode & 32) == 0 && (prm.mode & 3) != 2 && prm.input_mu == 52) {
+            // norm lean window: P1_W exponents (keys b, b + 2, .., b + 2 P1_W - 2), the
+            // start maximising the sampled coverage among windows holding no sampled key
+            // whose estimated score could reach HALF / SINGLE (those stay in the cold
+            // path, which computes the exact variants).  eps_eff is bounded with the
+            // number of sampled keys under per-bin splitting (n_bins >= that number).
+            constexpr int PER = (KEYS + P1_T - 1) / P1_T;
+            constexpr int SPAN = 2 * P1_W - 1;
+            uint32_t* upref = hist + 8448;                                  // KEYS+1 u32
+            const int lane = tid & 31, warp = tid >> 5;
+            const uint32_t ns = pref[KEYS];
+            uint32_t nk = 0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int k = tid * PER + i;
+                nk += (k < KEYS && hist[k]) ? 1u : 0u;
+            }
+            nk = __reduce_add_sync(0xffffffffu, nk);
+            if (lane == 0) S.red[warp] = nk;
+            __syncthreads();
+            uint32_t nkeys = 0;
+            for (int w = 0; w < P1_T / 32; ++w) nkeys += (uint32_t)S.red[w];
+            const double eps_e = prm.per_bin && nkeys > 1 ? prm.epsilon / (double)nkeys : prm.epsilon;
+            const int fl = flexp_bits(dbits(eps_e));
+            const bool check = (prm.mode & 3) == 0;
+            uint32_t loc[PER];
+            uint32_t run = 0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int k = tid * PER + i;
+                const uint32_t c = k < KEYS ? hist[k] : 0u;
+                uint32_t u = 0;
+                if (c && check) {
+                    const double mest = (double)c * (double)prm.n_total / (double)ns;
+                    const int lg = mest >= 1.0 ? flexp_bits(dbits(mest)) : 0;
+                    const int score = lg - 2 + (k - S.kmax) - fl + 1;
+                    u = (score > -6 && score < 27) ? 1u : 0u;
+                }
+                run += u;
+                loc[i] = run;
+            }
+            uint32_t incl = run;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            __syncthreads();
+            if (lane == 31) S.red[warp] = incl;
+            __syncthreads();
+            uint32_t pre = incl - run;
+            for (int w = 0; w < warp; ++w) pre += (uint32_t)S.red[w];
+            if (tid == 0) upref[0] = 0u;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int k = tid * PER + i;
+                if (k < KEYS) upref[k + 1] = pre + loc[i];
+            }
+            __syncthreads();
+            unsigned long long best = 0ull;
+            const int lo = P1_SAFE_LO + ((P1_SAFE_LO - KOFF) & 1);           // keys of x . x have KOFF's parity
+            for (int b = lo + 2 * tid; b + SPAN - 1 <= KOFF + 1021; b += 2 * P1_T) {
+                if (upref[b + SPAN] != upref[b]) continue;
+                const uint32_t cov = pref[b + SPAN] - pref[b];
+                const unsigned long long cand = ((unsigned long long)cov << 32) | (uint32_t)b;   // ties: larger b
+                best = cand > best ? cand : best;
+            }
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+                best = t > best ? t : best;
+            }
+            __syncthreads();
+            if (lane == 0) S.red[warp] = best;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long m = 0ull;
+                for (int w = 0; w < P1_T / 32; ++w) m = S.red[w] > m ? S.red[w] : m;
+                const uint32_t cov = (uint32_t)(m >> 32);
+                // worth it when the window holds >= 7/8 of the sample (the rest goes
+                // through the cold-element queue)
+                if (ns && (uint64_t)cov * 8u >= (uint64_t)ns * 7u) {
+                    const int b = (int)(uint32_t)m;
+                    S.norm_lean = 1;
+                    S.full = 0;
+                    S.wide = 0;
+                    S.queue = 1;
+                    S.base = b;
+                    int cb = b - (P1_CW - SPAN) / 2;
+                    cb = cb < 0 ? 0 : cb;
+                    S.cbase = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
+                }
+            }
+            __syncthreads();
+        }
     }
     // ---- clear private slots, cold table and totals
     for (int k = tid; k < P1_W * P1_T; k += P1_T) S.priv[k] = make_ulonglong2(0ull, 0ull);
@@ -677,6 +847,8 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     const bool fullmode = SMALL || S.full != 0;
     if (SMALL) {
         p1_main<NORM, VEC, true, false, V, false, 0>(S, x, y, n, A, B, tid, &zc, &nf);
+    } else if (NORM && S.norm_lean) {
+        p1_main_norm<VEC, V, L2D>(S, x, n, A, B, tid, &zc, &nf);
     } else if (S.wide) {
         if (S.queue) p1_main<NORM, VEC, false, true, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
         else p1_main<NORM, VEC, false, false, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
@@ -689,11 +861,13 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     }
 
     // ---- publish CTA partials (the cold table was pushed by the last flush)
+    const int kstep = (NORM && S.norm_lean) ? 2 : 1;
     for (int r = tid; r < (S.wide ? P1_WW : P1_W); r += P1_T) {
         if (S.t_c[r]) {
-            push_key(A, B, S.base + r, (unsigned long long)S.t_c[r], S.t_d[r], S.t_s[r], S.t_h[r]);
-            atomicAdd(reinterpret_cast<unsigned long long*>(A + A_PRIV + S.base + r), (unsigned long long)S.t_c[r]);
-            if (!fullmode) atomicAdd(reinterpret_cast<unsigned long long*>(A + A_HOT + S.base + r),
+            const int key = S.base + kstep * r;
+            push_key(A, B, key, (unsigned long long)S.t_c[r], S.t_d[r], S.t_s[r], S.t_h[r]);
+            atomicAdd(reinterpret_cast<unsigned long long*>(A + A_PRIV + key), (unsigned long long)S.t_c[r]);
+            if (!fullmode) atomicAdd(reinterpret_cast<unsigned long long*>(A + A_HOT + key),
                                      (unsigned long long)S.t_c[r]);
         }
     }

@@ -98,9 +98,9 @@ def check_against_golden(case, rep):
 CASES = G.select(max_n=1 << 20)
 
 
-@pytest.fixture(params=[0, 1, 2, 1 | 4, 2 | 4, 2 | 8, 1 | 16, 1 | 4 | 16],
+@pytest.fixture(params=[0, 1, 2, 1 | 4, 2 | 4, 2 | 8, 1 | 16, 1 | 4 | 16, 32, 1 | 32],
                 ids=["auto", "lean", "full", "lean-queue", "full-queue", "full-noqueue", "lean-wide",
-                     "lean-wide-queue"])
+                     "lean-wide-queue", "auto-nonormloop", "lean-nonormloop"])
 def pass1_mode(request, monkeypatch):
     from paper_2105_00115_b200 import device
     monkeypatch.setattr(device, "PASS1_MODE", request.param)
