@@ -471,7 +471,7 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
 // safe range, so rel < P1_W also excludes zero / subnormal / non-finite x.
 // Returns the tile's cold elements (bit j: xv[j] outside the window).
 template <int V, bool FULLT>
-__device__ __forceinline__ uint32_t p1_tile_norm(char* __restrict__ myb, uint32_t ebase, const double (&xv)[2 * V],
+__device__ __forceinline__ uint32_t p1_tile_norm(uint32_t mys, uint32_t ebase, const double (&xv)[2 * V],
                                                  int64_t e0, int64_t n, int tid) {
     uint32_t cold = 0;
 #pragma unroll
@@ -479,27 +479,35 @@ __device__ __forceinline__ uint32_t p1_tile_norm(char* __restrict__ myb, uint32_
         const uint32_t hi = (uint32_t)__double2hiint(xv[j]);
         const uint32_t d = (hi & 0x7FF00000u) - ebase;          // (slot of x's exponent) << 20
         const bool ok = FULLT || e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1) < n;
-        const double m26 = __hiloint2double((int)((hi & 0x000FFFFFu) | 0x41900000u), __double2loint(xv[j]));
+        uint32_t mh;                                             // (hi & 0xFFFFF) | 0x41900000 in one LOP3
+        asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(mh) : "r"(hi), "r"(0x000FFFFFu), "r"(0x41900000u));
+        const double m26 = __hiloint2double((int)mh, __double2loint(xv[j]));
         const long long kd = __double2ll_rn(__dmul_rn(m26, m26));
-        if (d < ((uint32_t)P1_W << 20)) {
-            if (ok) {
-                ulonglong2* slot = reinterpret_cast<ulonglong2*>(myb + (d >> 8));   // slot * P1_T * 16 bytes
-                ulonglong2 v = *slot;
-                v.x += (unsigned long long)kd;
-                v.y += 1ull;
-                *slot = v;
-            }
-        } else if (ok) {
-            cold |= 1u << j;
-        }
+        const bool hot = d < ((uint32_t)P1_W << 20);
+        // slot {D lo, D hi, count, 0} at mys + slot * P1_T * 16 bytes.  Straight-line code
+        // (no per-element branch / reconvergence): every element loads a slot (a cold one
+        // reads slot (d mod P1_W), harmlessly) and only a window element stores it back
+        asm volatile("{\n\t.reg .pred p;\n\t.reg .u32 a, b, c, w;\n\t"
+                     "setp.ne.u32 p, %3, 0;\n\t"
+                     "ld.shared.v4.u32 {a, b, c, w}, [%0];\n\t"
+                     "add.cc.u32 a, a, %1;\n\t"
+                     "addc.u32 b, b, %2;\n\t"
+                     "add.u32 c, c, 1;\n\t"
+                     "@p st.shared.v4.u32 [%0], {a, b, c, w};\n\t}"
+                     :: "r"(mys + ((d & (((uint32_t)P1_W - 1u) << 20)) >> 8)), "r"((uint32_t)kd),
+                        "r"((uint32_t)((unsigned long long)kd >> 32)), "r"((uint32_t)(hot && ok)));
+        // (no memory clobber: it would force the tile's registers into local memory; the
+        // slots are touched by C++ code only across __syncthreads, and volatile asm keeps
+        // its order)
+        if (!hot && ok) cold |= 1u << j;
     }
     return cold;
 }
 
-template <bool VEC, int V, int L2D>
+template <bool VEC, int V>
 __device__ __forceinline__ void p1_main_norm(P1Shared& S, const double* __restrict__ x, int64_t n,
                                              int64_t* __restrict__ A, int64_t* __restrict__ B, int tid,
-                                             uint32_t* zc, uint32_t* nf) {
+                                             uint32_t* zc, uint32_t* nf, int L2D) {
     constexpr int EPT = 2 * V;
     constexpr int TILE = P1_T * EPT;
     constexpr int FLUSH = 511 / EPT;                   // D < 511 * 2^54 per slot between flushes
@@ -507,7 +515,7 @@ __device__ __forceinline__ void p1_main_norm(P1Shared& S, const double* __restri
     const int64_t stride = gridDim.x;
     // slot r holds key base + 2r, i.e. biased exponent fx = r + (base - KOFF) / 2 + 1023
     const uint32_t ebase = (uint32_t)((S.base - KOFF) / 2 + 1023) << 20;
-    char* __restrict__ myb = reinterpret_cast<char*>(S.priv + tid);
+    const uint32_t mys = (uint32_t)__cvta_generic_to_shared(S.priv + tid);
     const int warp = tid >> 5, lane = tid & 31;
     int since = 0;
     uint32_t qn = 0;
@@ -519,12 +527,13 @@ __device__ __forceinline__ void p1_main_norm(P1Shared& S, const double* __restri
         bool f;
         if (L2D > 0 && tid == 0) p1_prefetch_l2<true>(x, x, n, t + (L2D + 1) * stride, TILE);
         p1_load<true, VEC, V>(x, x, n, t, tid, xv, yv, f);
-        const uint32_t cold = f ? p1_tile_norm<V, true>(myb, ebase, xv, t * TILE, n, tid)
-                                : p1_tile_norm<V, false>(myb, ebase, xv, t * TILE, n, tid);
-        if (__any_sync(0xffffffffu, cold != 0u)) {
+        const uint32_t cold = f ? p1_tile_norm<V, true>(mys, ebase, xv, t * TILE, n, tid)
+                                : p1_tile_norm<V, false>(mys, ebase, xv, t * TILE, n, tid);
+        const uint32_t wm = __reduce_or_sync(0xffffffffu, cold);     // positions with a cold element in the warp
+        if (wm) {
 #pragma unroll
             for (int j = 0; j < EPT; ++j)
-                p1_enqueue(S, A, B, warp, lane, qn, (cold >> j) & 1u, xv[j], xv[j], zc, nf);
+                if ((wm >> j) & 1u) p1_enqueue(S, A, B, warp, lane, qn, (cold >> j) & 1u, xv[j], xv[j], zc, nf);
         }
         if (++since == FLUSH) {
             p1_drain(S, A, B, warp, lane, qn, zc, nf);
@@ -774,8 +783,11 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                 if (c && check) {
                     const double mest = (double)c * (double)prm.n_total / (double)ns;
                     const int lg = mest >= 1.0 ? flexp_bits(dbits(mest)) : 0;
+                    // the sampled kmax undershoots e_max and the sampled key count n_bins
+                    // (score overestimated / underestimated by about as much), so the
+                    // margin to 23 (SINGLE) covers the count's sampling noise
                     const int score = lg - 2 + (k - S.kmax) - fl + 1;
-                    u = (score > -6 && score < 27) ? 1u : 0u;
+                    u = (score > -6 && score < 25) ? 1u : 0u;
                 }
                 run += u;
                 loc[i] = run;
@@ -848,7 +860,11 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
     if (SMALL) {
         p1_main<NORM, VEC, true, false, V, false, 0>(S, x, y, n, A, B, tid, &zc, &nf);
     } else if (NORM && S.norm_lean) {
-        p1_main_norm<VEC, V, L2D>(S, x, n, A, B, tid, &zc, &nf);
+        // L2 prefetch distance in tiles (a norm tile is half the bytes of an x . y tile);
+        // mode bits 6-7 select it for tuning: 0 -> 2 L2D + 1, 1 -> L2D, 2 -> none, 3 -> 1
+        const int sel = (prm.mode >> 6) & 3;
+        const int l2d = L2D == 0 ? 0 : (sel == 0 ? 2 * L2D + 1 : (sel == 1 ? L2D : (sel == 2 ? 0 : 1)));
+        p1_main_norm<VEC, V>(S, x, n, A, B, tid, &zc, &nf, l2d);
     } else if (S.wide) {
         if (S.queue) p1_main<NORM, VEC, false, true, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
         else p1_main<NORM, VEC, false, false, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
