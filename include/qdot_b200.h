@@ -140,7 +140,7 @@ int qdot_b200_begin(void* ws, void* stream);
  * cfg->reserved bits 0-1: 0 auto, 1 lean, 2 full; bits 2-3: cold-element warp
  * queue 0 auto, 4 on, 8 off; bit 4 (16): force the 24-key wide lean window;
  * bit 5 (32): norm mode without its exponent-indexed lean loop; bits 6-7: that
- * loop's L2 prefetch distance (tuning). */
+ * loop's L2 prefetch distance, bits 8-9 its cache policy (tuning). */
 int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
                     int64_t n_total, void* ws, void* stream);
 /* one-CTA scoring on the (reduced) histogram: partition, scores, precisions.

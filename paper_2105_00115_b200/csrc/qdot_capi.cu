@@ -142,9 +142,11 @@ int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const
         prm.per_bin = cfg->split == 1 && cfg->strategy == QDOT_STRATEGY_EXACT;
         // bits 0-1: 0 auto, 1 lean, 2 full; bits 2-3: queue 0 auto, 4 on, 8 off; bit 4: wide lean window;
         // bit 5: norm mode without the exponent-indexed lean loop (A/B); bits 6-7: its L2 prefetch
-        // distance
+        // distance, bits 8-9 its cache policy
         prm.mode = cfg->reserved;
-        if (prm.mode < 0 || (prm.mode & 3) > 2 || ((prm.mode >> 2) & 3) > 2 || (prm.mode >> 8)) return QDOT_ERR_ARG;
+        if (prm.mode < 0 || (prm.mode & 3) > 2 || ((prm.mode >> 2) & 3) > 2 || ((prm.mode >> 8) & 3) > 2 ||
+            (prm.mode >> 10))
+            return QDOT_ERR_ARG;
     }
     WsPtrs w = ws_ptrs(ws);
     QD_CHECK(launch_pass1(x, norm ? x : y, n, norm != 0, w.a, w.b, prm, static_cast<cudaStream_t>(stream)), "pass1");

@@ -470,6 +470,14 @@ __device__ __forceinline__ void p1_main(P1Shared& S, const double* __restrict__ 
 // conversion give the DOUBLE units (emulate.py:133).  Window keys lie in the
 // safe range, so rel < P1_W also excludes zero / subnormal / non-finite x.
 // Returns the tile's cold elements (bit j: xv[j] outside the window).
+// L2 prefetch of one norm tile with an explicit cache policy (pol from createpolicy)
+__device__ __forceinline__ void p1_prefetch_norm(const double* x, int64_t n, int64_t tile, int TILE, uint64_t pol) {
+    const int64_t e0 = tile * TILE;
+    if (e0 + TILE > n) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(bulk_aligned(x + e0)),
+                 "r"(TILE * 8), "l"(pol) : "memory");
+}
+
 template <int V, bool FULLT>
 __device__ __forceinline__ uint32_t p1_tile_norm(uint32_t mys, uint32_t ebase, const double (&xv)[2 * V],
                                                  int64_t e0, int64_t n, int tid) {
@@ -504,43 +512,66 @@ __device__ __forceinline__ uint32_t p1_tile_norm(uint32_t mys, uint32_t ebase, c
     return cold;
 }
 
+// one norm tile: window elements into the private slots, cold ones through the
+// warp queue, the flush every FLUSH tiles
+template <int V>
+__device__ __forceinline__ void p1_norm_tile(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B,
+                                             uint32_t mys, uint32_t ebase, const double (&xv)[2 * V], int64_t t,
+                                             bool f, int64_t n, int tid, uint32_t& qn, int& since, uint32_t* zc,
+                                             uint32_t* nf) {
+    constexpr int EPT = 2 * V;
+    constexpr int FLUSH = 511 / EPT;                   // D < 511 * 2^54 per slot between flushes
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t cold = f ? p1_tile_norm<V, true>(mys, ebase, xv, t * (P1_T * EPT), n, tid)
+                            : p1_tile_norm<V, false>(mys, ebase, xv, t * (P1_T * EPT), n, tid);
+    const uint32_t wm = __reduce_or_sync(0xffffffffu, cold);     // positions with a cold element in the warp
+    if (wm) {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j)
+            if ((wm >> j) & 1u) p1_enqueue(S, A, B, warp, lane, qn, (cold >> j) & 1u, xv[j], xv[j], zc, nf);
+    }
+    if (++since == FLUSH) {
+        p1_drain(S, A, B, warp, lane, qn, zc, nf);
+        p1_flush<false, P1_W>(S, A, B, tid);
+        since = 0;
+    }
+}
+
+// (register double buffering -- the next tile's loads issued before the current
+// tile is accumulated -- and two tiles per iteration both measured slower:
+// 0.60 / 0.49 vs 0.45 ms at 2^28, profiles/r2_norm_experiments.md)
 template <bool VEC, int V>
 __device__ __forceinline__ void p1_main_norm(P1Shared& S, const double* __restrict__ x, int64_t n,
                                              int64_t* __restrict__ A, int64_t* __restrict__ B, int tid,
-                                             uint32_t* zc, uint32_t* nf, int L2D) {
+                                             uint32_t* zc, uint32_t* nf, int L2D, int pmode) {
     constexpr int EPT = 2 * V;
     constexpr int TILE = P1_T * EPT;
-    constexpr int FLUSH = 511 / EPT;                   // D < 511 * 2^54 per slot between flushes
     const int64_t ntiles = (n + TILE - 1) / TILE;
     const int64_t stride = gridDim.x;
     // slot r holds key base + 2r, i.e. biased exponent fx = r + (base - KOFF) / 2 + 1023
     const uint32_t ebase = (uint32_t)((S.base - KOFF) / 2 + 1023) << 20;
     const uint32_t mys = (uint32_t)__cvta_generic_to_shared(S.priv + tid);
-    const int warp = tid >> 5, lane = tid & 31;
     int since = 0;
     uint32_t qn = 0;
+    // prefetched lines: evict-first (0), evict-normal (1) or evict-last (2); the demand
+    // loads stream with evict-first either way
+    uint64_t pol = 0;
+    if (tid == 0) {
+        if (pmode == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        else if (pmode == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    }
     if (L2D > 0 && tid == 0) {
-        for (int d = 1; d <= L2D; ++d) p1_prefetch_l2<true>(x, x, n, blockIdx.x + d * stride, TILE);
+        for (int d = 1; d <= L2D; ++d) p1_prefetch_norm(x, n, blockIdx.x + d * stride, TILE, pol);
     }
     for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
         double xv[EPT], yv[EPT];
         bool f;
-        if (L2D > 0 && tid == 0) p1_prefetch_l2<true>(x, x, n, t + (L2D + 1) * stride, TILE);
+        if (L2D > 0 && tid == 0) p1_prefetch_norm(x, n, t + (L2D + 1) * stride, TILE, pol);
         p1_load<true, VEC, V>(x, x, n, t, tid, xv, yv, f);
-        const uint32_t cold = f ? p1_tile_norm<V, true>(mys, ebase, xv, t * TILE, n, tid)
-                                : p1_tile_norm<V, false>(mys, ebase, xv, t * TILE, n, tid);
-        const uint32_t wm = __reduce_or_sync(0xffffffffu, cold);     // positions with a cold element in the warp
-        if (wm) {
-#pragma unroll
-            for (int j = 0; j < EPT; ++j)
-                if ((wm >> j) & 1u) p1_enqueue(S, A, B, warp, lane, qn, (cold >> j) & 1u, xv[j], xv[j], zc, nf);
-        }
-        if (++since == FLUSH) {
-            p1_drain(S, A, B, warp, lane, qn, zc, nf);
-            p1_flush<false, P1_W>(S, A, B, tid);
-            since = 0;
-        }
+        p1_norm_tile<V>(S, A, B, mys, ebase, xv, t, f, n, tid, qn, since, zc, nf);
     }
+    const int warp = tid >> 5, lane = tid & 31;
     p1_drain(S, A, B, warp, lane, qn, zc, nf);
     p1_flush<false, P1_W>(S, A, B, tid);
 }
@@ -861,10 +892,10 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         p1_main<NORM, VEC, true, false, V, false, 0>(S, x, y, n, A, B, tid, &zc, &nf);
     } else if (NORM && S.norm_lean) {
         // L2 prefetch distance in tiles (a norm tile is half the bytes of an x . y tile);
-        // mode bits 6-7 select it for tuning: 0 -> 2 L2D + 1, 1 -> L2D, 2 -> none, 3 -> 1
+        // mode bits 6-7 select it for tuning: 0 -> L2D, 1 -> 2 L2D + 1, 2 -> none, 3 -> 1
         const int sel = (prm.mode >> 6) & 3;
-        const int l2d = L2D == 0 ? 0 : (sel == 0 ? 2 * L2D + 1 : (sel == 1 ? L2D : (sel == 2 ? 0 : 1)));
-        p1_main_norm<VEC, V>(S, x, n, A, B, tid, &zc, &nf, l2d);
+        const int l2d = L2D == 0 ? 0 : (sel == 0 ? L2D : (sel == 1 ? 2 * L2D + 1 : (sel == 2 ? 0 : 1)));
+        p1_main_norm<VEC, V>(S, x, n, A, B, tid, &zc, &nf, l2d, (prm.mode >> 8) & 3);
     } else if (S.wide) {
         if (S.queue) p1_main<NORM, VEC, false, true, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
         else p1_main<NORM, VEC, false, false, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
