@@ -143,6 +143,18 @@ int qdot_b200_begin(void* ws, void* stream);
  * loop's L2 prefetch distance, bits 8-9 its cache policy (tuning). */
 int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg,
                     int64_t n_total, void* ws, void* stream);
+/* the whole single-device pipeline of one qdot on `stream` (no sync): for
+ * 1 <= n <= 16384 with the exact strategy and cfg->reserved 0,
+ * one thread-block-cluster launch that keeps every exact per-key partial in
+ * distributed shared memory and scores / finalizes in place (qdot_b200_small),
+ * then score_finalize and pass2_finalize, which return at once unless it
+ * handed the call over; otherwise begin, pass1, score_finalize,
+ * pass2_finalize.  Replaces kernel.qdot's body (kernel.py:179-240). */
+int qdot_b200_enqueue(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                      void* stream);
+int qdot_b200_small(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                    void* stream);
+int64_t qdot_b200_small_max(void);   /* qdot_b200_small's limit (65536) */
 /* one-CTA scoring on the (reduced) histogram: partition, scores, precisions.
  * Replaces kernel.select_parameters' partition + scoring (kernel.py:59-72,
  * binning.py:191-284, scoring.py:126-216).  n_total = elements over all ranks. */
@@ -344,6 +356,15 @@ int qdot_b200_cg_xr(int64_t n, const void* ws_pq, double* st, double* x, const d
                     const double* q, void* stream);
 int qdot_b200_cg_p_check(int64_t n, const void* ws_pq, const void* ws_rr, double* st, const double* r, double* p,
                          void* rec, long long* counter, unsigned long long handle, void* stream);
+/* fused power-method iteration for the loop body (apps.py:302-315): pm_div:
+ * x_next = z / sqrt(c) (c = the z.z result in ws_zz; st[0] = c, st[3] = sqrt c);
+ * pm_check: x = x_next, then in the last CTA lam = (x . x_next) * st[3]
+ * (st[4], st[5] = lam_prev, st[6] = 1), the record of iteration k and the
+ * condition (both dots OK, z not all zero, z.z >= 0, not |lam - lam_prev| <=
+ * tau = st[7] with st[6] set on entry, k + 1 < cap); counter = {k, cap, ticket}. */
+int qdot_b200_pm_div(int64_t n, const void* ws_zz, double* st, const double* z, double* xn, void* stream);
+int qdot_b200_pm_check(int64_t n, const void* ws_zz, const void* ws_lam, double* st, const double* xn, double* x,
+                       void* rec, long long* counter, unsigned long long handle, void* stream);
 
 /* --- host-side helpers (no GPU needed; exported for tests and bindings) ----- */
 /* correctly rounded acc * 2^u with math.ldexp semantics; *overflow set on range error */

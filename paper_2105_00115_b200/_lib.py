@@ -11,6 +11,8 @@ import ctypes
 import os
 import threading
 
+import numpy as np
+
 from . import build as _build
 
 KEYS = 4195
@@ -55,6 +57,14 @@ class QdotWsLayout(ctypes.Structure):
 
 assert ctypes.sizeof(QdotBin) == 56
 
+# the same header as a numpy record, for bulk parsing of device-recorded iterations
+RESULT_DTYPE = np.dtype({"names": ["value", "eps_eff", "n", "nnz", "zero_count", "counts", "status", "n_bins"],
+                         "formats": ["<f8", "<f8", "<i8", "<i8", "<i8", ("<i8", (4,)), "<i4", "<i4"],
+                         "offsets": [QdotResult.value.offset, QdotResult.eps_eff.offset, QdotResult.n.offset,
+                          QdotResult.nnz.offset, QdotResult.zero_count.offset, QdotResult.counts.offset,
+                          QdotResult.status.offset, QdotResult.n_bins.offset],
+                         "itemsize": ctypes.sizeof(QdotResult)})
+
 _lock = threading.Lock()
 _lib = None
 
@@ -70,6 +80,9 @@ SIGNATURES = {
     "qdot_b200_workspace_layout": (_I, [ctypes.POINTER(QdotWsLayout)]),
     "qdot_b200_device_info": (_I, [ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "qdot_b200_begin": (_I, [_P, _P]),
+    "qdot_b200_enqueue": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _P, _P]),
+    "qdot_b200_small": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _P, _P]),
+    "qdot_b200_small_max": (_I64, []),
     "qdot_b200_pass1": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _I64, _P, _P]),
     "qdot_b200_score": (_I, [_P, _I64, ctypes.POINTER(QdotConfig), _P]),
     "qdot_b200_score_finalize": (_I, [_P, _I64, ctypes.POINTER(QdotConfig), _P]),
@@ -99,6 +112,8 @@ SIGNATURES = {
     "qdot_b200_acg_check": (_I, [_P, _P, _P, _P, _P, ctypes.c_ulonglong, _P]),
     "qdot_b200_cg_xr": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P]),
     "qdot_b200_cg_p_check": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_ulonglong, _P]),
+    "qdot_b200_pm_div": (_I, [_I64, _P, _P, _P, _P, _P]),
+    "qdot_b200_pm_check": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_ulonglong, _P]),
     "qdot_b200_exact_workspace_bytes": (ctypes.c_size_t, []),
     "qdot_b200_exact_region_words": (_I64, []),
     "qdot_b200_exact_begin": (_I, [_P, _P]),

@@ -18,12 +18,14 @@ as the reference on the host; they are input preparation, not the hot path.
 reference_cg / reference_pm are the plain-double baselines (torch on the
 device), kept for iteration-count comparisons like the reference's.
 
-Solves with at least GRAPH_MIN unknowns run every iteration as one CUDA graph
-(SpMV, both qdot pipelines, the scalar recurrence on the device -- alpha,
-beta, sqrt with IEEE division / square root, i.e. the Python float values --
-and the vector updates), whose last node publishes both qdot result headers
-into pinned host memory: one host wake-up per iteration instead of two
-synchronising qdot calls plus separate launches.
+Solves with at least GRAPH_MIN unknowns run their iterations on the device:
+one CUDA graph whose WHILE-conditional node repeats a captured iteration
+(SpMV, both qdot pipelines, fused kernels for the scalar recurrence -- alpha,
+beta, sqrt, lambda with IEEE division / square root / product, i.e. the
+Python float values -- and the vector updates) and ends with a check kernel
+that records the iteration (both qdot result headers and the scalars) and
+stops the loop where the host loop would; the host parses the records once
+per solve, raises the same errors and builds the same trace.
 """
 
 from __future__ import annotations
@@ -330,7 +332,7 @@ class PMResult:
 
 
 # --------------------------------------------------------------------------- graph iterations
-GRAPH_MIN = 2048          # solves of at least this many unknowns run each iteration as one CUDA graph
+GRAPH_MIN = 2048          # solves of at least this many unknowns run their iterations in the device loop
 GRAPH_REPEAT = True       # smaller ones too from their second solve on the same matrix and configuration
                           # (a capture costs ~2-3 ms: worth it once the graph is replayed by later solves)
 
@@ -376,10 +378,10 @@ def _graph_entry(a: "SparseMatrix", key) -> Optional[_GraphEntry]:
 
 
 class _IterGraph:
-    """Device resources of graph-captured solver iterations: two qdot
+    """Device resources of a solver's device-resident iteration loop: two qdot
     workspaces (one per dot product of an iteration), the scalar state st[8],
-    and a pinned, device-visible host block the last node publishes into
-    (two 256-byte result headers, st, then a sequence word)."""
+    the loop graph (a WHILE-conditional node around one captured iteration)
+    and its per-iteration record buffer (two 256-byte result headers and st)."""
 
     def __init__(self, device):
         torch, _ = _dev()
@@ -388,43 +390,29 @@ class _IterGraph:
         self.lib = lib
         self.ws = [torch.empty(nb, dtype=torch.uint8, device=device) for _ in range(2)]
         self.st = torch.zeros(8, dtype=torch.float64, device=device)
-        self.seq_dev = torch.zeros(1, dtype=torch.int32, device=device)
-        self.host_t = torch.zeros(640, dtype=torch.uint8).pin_memory()
-        self.host = self.host_t.numpy()
-        self.seq_view = self.host[576:580].view(np.uint32)
-        self.seen = 0
-        self.graphs = []
 
     def qdot_nodes(self, k: int, xd, yd, norm: bool, c, stream: int) -> None:
         """The qdot pipeline into workspace k (stream-ordered, no host sync)."""
         lib, ws, n = self.lib, self.ws[k].data_ptr(), int(xd.shape[0])
         xp = xd.data_ptr()
         yp = xp if norm else yd.data_ptr()
-        _lib.check(lib.qdot_b200_begin(ws, stream), lib)
-        _lib.check(lib.qdot_b200_pass1(xp, yp, n, int(norm), ctypes.byref(c), n, ws, stream), lib)
-        _lib.check(lib.qdot_b200_score_finalize(ws, n, ctypes.byref(c), stream), lib)
-        _lib.check(lib.qdot_b200_pass2_finalize(xp, yp, n, int(norm), ws, stream), lib)
+        # begin / pass 1 / score / pass 2, or the one-launch cluster path at small n
+        _lib.check(lib.qdot_b200_enqueue(xp, yp, n, int(norm), ctypes.byref(c), ws, stream), lib)
 
-    def update(self, op: int, a, si: int, b, out, stream: int) -> None:
-        """out = a + st[si]*b | a - st[si]*b | a / st[si]."""
-        sp = self.st.data_ptr() + 8 * si
-        _lib.check(self.lib.qdot_b200_vec_update_dev(a.shape[0], op, a.data_ptr(), sp,
-                                                     b.data_ptr() if b is not None else None, out.data_ptr(),
-                                                     stream), self.lib)
-
-    def scalar(self, which: int, k: int, stream: int) -> None:
-        _lib.check(self.lib.qdot_b200_solver_scalar(which, self.ws[k].data_ptr(), self.st.data_ptr(), stream),
-                   self.lib)
-
-    # ---- device-resident loop (ACG): a WHILE-conditional graph whose body is
-    # one iteration ending with qdot_b200_acg_check (records the iteration,
-    # sets the loop condition); one launch and one host wake-up per solve
+    # ---- device-resident loop: a WHILE-conditional graph whose body is one
+    # iteration ending with a check kernel (qdot_b200_cg_p_check for ACG,
+    # qdot_b200_pm_check for APM: records the iteration, sets the loop
+    # condition); one launch and one host wake-up per solve
     LOOP_CAP = 4096                                           # iterations per launch (record buffer)
 
-    def check(self, handle: int, stream: int) -> None:
-        _lib.check(self.lib.qdot_b200_acg_check(self.ws[0].data_ptr(), self.ws[1].data_ptr(), self.st.data_ptr(),
-                                                self.rec.data_ptr(), self.ctr.data_ptr(), handle, stream),
-                   self.lib)
+    def pm_div(self, z, xn, stream: int) -> None:
+        _lib.check(self.lib.qdot_b200_pm_div(z.shape[0], self.ws[0].data_ptr(), self.st.data_ptr(), z.data_ptr(),
+                                             xn.data_ptr(), stream), self.lib)
+
+    def pm_check(self, xn, x, handle: int, stream: int) -> None:
+        _lib.check(self.lib.qdot_b200_pm_check(x.shape[0], self.ws[0].data_ptr(), self.ws[1].data_ptr(),
+                                               self.st.data_ptr(), xn.data_ptr(), x.data_ptr(), self.rec.data_ptr(),
+                                               self.ctr.data_ptr(), handle, stream), self.lib)
 
     def cg_xr(self, x, p, r, q, stream: int) -> None:
         _lib.check(self.lib.qdot_b200_cg_xr(x.shape[0], self.ws[0].data_ptr(), self.st.data_ptr(), x.data_ptr(),
@@ -456,9 +444,13 @@ class _IterGraph:
             _lib.check(self.lib.qdot_b200_loop_finish(loop, side.cuda_stream), self.lib)
         torch.cuda.current_stream().wait_stream(side)
 
+    REC_DTYPE = np.dtype({"names": ["a", "b", "st"], "formats": [_lib.RESULT_DTYPE, _lib.RESULT_DTYPE, ("<f8", (8,))],
+                          "offsets": [0, 256, 512], "itemsize": 576})
+
     def run_loop(self, cap: int, tau: float):
         """Run up to `cap` iterations on the device (st[0] = c set by the
-        caller); returns [(result header of ws 0, of ws 1, st)] per iteration."""
+        caller); returns the recorded iterations as a numpy record array
+        (fields a / b: the two dots' result headers, st: the scalar state)."""
         torch, _ = _dev()
         stream = torch.cuda.current_stream()
         self.st[7] = tau
@@ -468,14 +460,12 @@ class _IterGraph:
         self.ctr.copy_(self.ctr_host, non_blocking=True)
         _lib.check(self.lib.qdot_b200_loop_launch(self.loop, stream.cuda_stream), self.lib)
         k = int(self.ctr[0].item())                       # waits for the loop
-        buf = self.rec[:k * 576].cpu().numpy().tobytes()
-        out = []
-        for i in range(k):
-            b = buf[i * 576:(i + 1) * 576]
-            out.append((_lib.QdotResult.from_buffer_copy(b[0:ctypes.sizeof(_lib.QdotResult)]),
-                        _lib.QdotResult.from_buffer_copy(b[256:256 + ctypes.sizeof(_lib.QdotResult)]),
-                        np.frombuffer(b[512:576], dtype=np.float64)))
-        return out
+        return np.frombuffer(self.rec[:k * 576].cpu().numpy().tobytes(), dtype=self.REC_DTYPE, count=k)
+
+    def header(self, rec, field: str, i: int):
+        """Record i's result header `field` as a QdotResult (error paths)."""
+        raw = rec[field][i:i + 1].tobytes()
+        return _lib.QdotResult.from_buffer_copy(raw + bytes(ctypes.sizeof(_lib.QdotResult) - len(raw)))
 
     def __del__(self):
         loop = getattr(self, "loop", None)
@@ -484,52 +474,6 @@ class _IterGraph:
                 self.lib.qdot_b200_loop_destroy(loop)
             except Exception:
                 pass
-
-    def publish(self, stream: int) -> None:
-        _lib.check(self.lib.qdot_b200_publish_iter(self.ws[0].data_ptr(), self.ws[1].data_ptr(), self.st.data_ptr(),
-                                                   self.host_t.data_ptr(), self.seq_dev.data_ptr(), stream),
-                   self.lib)
-
-    def capture(self, body):
-        """Capture `body(stream)` as a CUDA graph on a side stream (nothing runs
-        yet; the launchers' one-time attribute setup is legal during capture).
-        capture_begin/end directly: the torch.cuda.graph context manager would
-        also gc.collect() and empty the caching allocator on every capture."""
-        torch, _ = _dev()
-        self.seen = int(self.seq_view[0])
-        g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            # thread-local capture mode: another thread's solve or qdot call
-            # (allocations, stream queries, syncs) neither invalidates this
-            # capture nor fails because of it
-            g.capture_begin(capture_error_mode="thread_local")
-            try:
-                body(side.cuda_stream)
-            finally:
-                g.capture_end()
-        torch.cuda.current_stream().wait_stream(side)
-        self.graphs.append(g)
-        return g
-
-    def run(self, g):
-        """Replay one iteration and wait for its published block; returns
-        (result header of workspace 0, of workspace 1, st[0..7])."""
-        g.replay()
-        self.seen = (self.seen + 1) & 0xFFFFFFFF
-        torch, _ = _dev()
-        spins = 0
-        while int(self.seq_view[0]) != self.seen:
-            spins += 1
-            if spins & 0xFFFF == 0 and torch.cuda.current_stream().query():
-                if int(self.seq_view[0]) != self.seen:
-                    raise RuntimeError("solver iteration did not publish its result")
-        buf = bytes(self.host[:576])
-        r0 = _lib.QdotResult.from_buffer_copy(buf[0:ctypes.sizeof(_lib.QdotResult)])
-        r1 = _lib.QdotResult.from_buffer_copy(buf[256:256 + ctypes.sizeof(_lib.QdotResult)])
-        st = np.frombuffer(buf[512:576], dtype=np.float64)
-        return r0, r1, st
 
 
 def _dot_report(res) -> "_DotReport":
@@ -617,19 +561,27 @@ def _acg(a, b, x0, tau, max_iters, cfg, strategy, torch, device, n, use_graph, e
                 entry.G, entry.graphs, entry.bufs = G, None, (x, r, p, q)
         G.st[0] = c
         while resid > tau and k < max_iters:
-            for r_pq, r_rr, st in G.run_loop(min(max_iters - k, G.LOOP_CAP), tau):
-                d_rep = _dot_report(r_pq)
-                d = d_rep.value
+            rec = G.run_loop(min(max_iters - k, G.LOOP_CAP), tau)
+            # the host loop's checks and trace rows, from the parsed records in bulk
+            a, b = rec["a"], rec["b"]
+            sa, va, ca, na = a["status"].tolist(), a["value"].tolist(), a["counts"].tolist(), a["n"].tolist()
+            sb, vb, cb, nb_ = b["status"].tolist(), b["value"].tolist(), b["counts"].tolist(), b["n"].tolist()
+            rows = trace.rows
+            for i in range(len(sa)):
+                if sa[i] != _lib.QDOT_OK:
+                    _dot_report(G.header(rec, "a", i))                # raises the call's error
+                d = va[i]
                 if not math.isfinite(d) or d <= 0.0:
                     raise BreakdownError(f"p.Ap = {d!r} at iteration {k}")
-                c_rep = _dot_report(r_rr)
-                if not (c_rep.value >= 0.0):                  # apps.py:171-175
+                if sb[i] != _lib.QDOT_OK:
+                    _dot_report(G.header(rec, "b", i))
+                c = vb[i]
+                if not (c >= 0.0):                                    # apps.py:171-175
                     raise AssertionError("norm computed by qdot must be nonnegative")
-                c = c_rep.value
                 resid = math.sqrt(c)
                 k += 1
-                trace.record(k, "pAp", d_rep, resid)
-                trace.record(k, "rtr", c_rep, resid)
+                rows.append(TraceRow(k, "pAp", dict(zip(LEVELS_ASC, ca[i])), na[i], resid))
+                rows.append(TraceRow(k, "rtr", dict(zip(LEVELS_ASC, cb[i])), nb_[i], resid))
     while resid > tau and k < max_iters:
         a.matvec_device(p, out=q)
         d_rep = dots(p, q, False)
@@ -689,48 +641,55 @@ def _apm(a, x_h, nrm, tau, max_iters, cfg, strategy, torch, device, use_graph, e
     k = 0
     converged = False
     if use_graph:
-        # two CUDA graphs (the x / x_next buffers swap roles every iteration):
-        # SpMV, z.z, s = sqrt(z.z), x_next = z / s, x.x_next, publish
-        bufs = (x, x_next)
+        # the iterations run on the device: one CUDA graph whose WHILE node
+        # repeats SpMV (z = A x), z.z, x_next = z / sqrt(z.z), x.x_next and the
+        # check node (x = x_next, lam, record, convergence); one launch and one
+        # host wake-up per solve (or per LOOP_CAP iterations)
         if cached:
-            G, graphs = entry.G, entry.graphs
+            G = entry.G
         else:
             G = _IterGraph(device)
             cst = config_struct(cfg, strategy)
 
-            def body_for(cur, nxt):
-                def body(stream):
-                    a.matvec_device(cur, out=z)
-                    G.qdot_nodes(0, z, z, True, cst, stream)
-                    G.scalar(2, 0, stream)                      # st[0] = z.z, st[3] = sqrt(z.z)
-                    G.update(_DIV, z, 3, None, nxt, stream)     # x_next = z / s
-                    G.qdot_nodes(1, cur, nxt, False, cst, stream)
-                    G.publish(stream)
-                return body
+            def body(stream, handle):
+                a.matvec_device(x, out=z)
+                G.qdot_nodes(0, z, z, True, cst, stream)
+                G.pm_div(z, x_next, stream)                     # x_next = z / sqrt(z.z)
+                G.qdot_nodes(1, x, x_next, False, cst, stream)
+                G.pm_check(x_next, x, handle, stream)           # x = x_next; lam; record; go on?
 
             a.device_arrays()                                   # host->device copies cannot be captured
             a.sell_arrays()
-            graphs = [G.capture(body_for(bufs[0], bufs[1])), G.capture(body_for(bufs[1], bufs[0]))]
+            G.capture_loop(body)
             if entry is not None:
-                entry.G, entry.graphs, entry.bufs = G, graphs, (x, x_next, z)
-        while k < max_iters:
-            r_zz, r_lam, _st = G.run(graphs[k % 2])
-            c_rep = _dot_report(r_zz)
-            if c_rep.zero_count == c_rep.n:
-                raise ZeroIterateError(f"A x vanished at iteration {k}")
-            if not (c_rep.value >= 0.0):                      # apps.py:171-175
-                raise AssertionError("norm computed by qdot must be nonnegative")
-            s_ = math.sqrt(c_rep.value)
-            lam_rep = _dot_report(r_lam)
-            lam = lam_rep.value * s_
-            k += 1
-            trace.record(k, "norm", c_rep, lam)
-            trace.record(k, "lambda", lam_rep, lam)
-            if lam_prev is not None and abs(lam - lam_prev) <= tau:
-                converged = True
-                break
-            lam_prev = lam
-        x = bufs[k % 2]
+                entry.G, entry.graphs, entry.bufs = G, None, (x, x_next, z)
+        while k < max_iters and not converged:
+            G.st[5] = 0.0 if lam_prev is None else lam_prev
+            G.st[6] = 0.0 if lam_prev is None else 1.0
+            rec = G.run_loop(min(max_iters - k, G.LOOP_CAP), tau)
+            ra, rb = rec["a"], rec["b"]
+            sa, va, ca, na, za = (ra["status"].tolist(), ra["value"].tolist(), ra["counts"].tolist(),
+                                  ra["n"].tolist(), ra["zero_count"].tolist())
+            sb, vb, cb, nb_ = rb["status"].tolist(), rb["value"].tolist(), rb["counts"].tolist(), rb["n"].tolist()
+            rows = trace.rows
+            for i in range(len(sa)):
+                if sa[i] != _lib.QDOT_OK:
+                    _dot_report(G.header(rec, "a", i))                # raises the call's error
+                if za[i] == na[i]:
+                    raise ZeroIterateError(f"A x vanished at iteration {k}")
+                if not (va[i] >= 0.0):                                # apps.py:171-175
+                    raise AssertionError("norm computed by qdot must be nonnegative")
+                s_ = math.sqrt(va[i])
+                if sb[i] != _lib.QDOT_OK:
+                    _dot_report(G.header(rec, "b", i))
+                lam = vb[i] * s_
+                k += 1
+                rows.append(TraceRow(k, "norm", dict(zip(LEVELS_ASC, ca[i])), na[i], lam))
+                rows.append(TraceRow(k, "lambda", dict(zip(LEVELS_ASC, cb[i])), nb_[i], lam))
+                if lam_prev is not None and abs(lam - lam_prev) <= tau:
+                    converged = True
+                    break
+                lam_prev = lam
         return PMResult(eigenvalue=lam, x=x.cpu().numpy(), iterations=k, converged=converged, trace=trace)
     while k < max_iters:
         a.matvec_device(x, out=z)

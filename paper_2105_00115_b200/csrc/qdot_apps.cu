@@ -257,6 +257,64 @@ __global__ void __launch_bounds__(T) k_cg_p_check(int64_t n, const void* ws_pq, 
     }
 }
 
+// ---- fused power-method iteration kernels for the device loop (apps.py:302-315)
+// x_next = z / s with s = sqrt(c), c = the z.z result in ws_zz (numpy z / s);
+// block 0 records c and s in st[0], st[3]
+__global__ void __launch_bounds__(T) k_pm_div(int64_t n, const void* ws_zz, double* st, const double* __restrict__ z,
+                                              double* __restrict__ xn) {
+    const double c = result_value(ws_zz);
+    const double sq = __dsqrt_rn(c);
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += (int64_t)gridDim.x * T)
+        xn[i] = __ddiv_rn(z[i], sq);
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st[0] = c; st[3] = sq; }
+}
+
+// x = x_next (the iterate for the next iteration); the last CTA computes
+// lam = (x . x_next) * s (the host's lam_rep.value * s_), records the iteration
+// and keeps looping while the host loop would: both dots OK, z not all zero,
+// z.z >= 0, not (a previous lam and |lam - lam_prev| <= tau), k + 1 < cap.
+// st: [0] c, [3] s, [4] lam, [5] lam_prev, [6] 1 when lam_prev exists, [7] tau.
+__global__ void __launch_bounds__(T) k_pm_check(int64_t n, const void* ws_zz, const void* ws_lam, double* st,
+                                                const double* __restrict__ xn, double* __restrict__ x,
+                                                unsigned char* rec, long long* counter,
+                                                cudaGraphConditionalHandle handle) {
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += (int64_t)gridDim.x * T) x[i] = xn[i];
+    __threadfence();
+    __syncthreads();
+    __shared__ int last;
+    if (threadIdx.x == 0)
+        last = atomicAdd(reinterpret_cast<unsigned long long*>(counter + 2), 1ull) == (unsigned long long)gridDim.x - 1ull;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int t = threadIdx.x;
+    const long long k = counter[0], cap = counter[1];
+    const qdot_result* r0 = reinterpret_cast<const qdot_result*>(static_cast<const char*>(ws_zz) + qd::OFF_RESULT);
+    const qdot_result* r1 = reinterpret_cast<const qdot_result*>(static_cast<const char*>(ws_lam) + qd::OFF_RESULT);
+    __shared__ bool go;
+    if (t == 0) {
+        const double lam = __dmul_rn(r1->value, st[3]);
+        const bool conv = st[6] != 0.0 && fabs(__dsub_rn(lam, st[5])) <= st[7];
+        go = r0->status == QDOT_OK && r0->zero_count != r0->n && r0->value >= 0.0 && r1->status == QDOT_OK &&
+             !conv && k + 1 < cap;
+        st[4] = lam;
+        st[5] = lam;
+        st[6] = 1.0;
+    }
+    __syncthreads();
+    const uint32_t* ra = reinterpret_cast<const uint32_t*>(r0);
+    const uint32_t* rb = reinterpret_cast<const uint32_t*>(r1);
+    uint32_t* h = reinterpret_cast<uint32_t*>(rec + k * REC_BYTES);
+    if (t < 64) h[t] = ra[t];
+    else if (t < 128) h[t] = rb[t - 64];
+    else if (t < 144) h[t] = reinterpret_cast<const uint32_t*>(st)[t - 128];
+    if (t == 0) {
+        counter[0] = k + 1;
+        counter[2] = 0;
+        cudaGraphSetConditional(handle, go ? 1u : 0u);
+    }
+}
+
 struct SolverLoop {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -339,6 +397,25 @@ int qdot_b200_cg_p_check(int64_t n, const void* ws_pq, const void* ws_rr, double
                                                                   (cudaGraphConditionalHandle)handle);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "cg_p_check");
+}
+
+int qdot_b200_pm_div(int64_t n, const void* ws_zz, double* st, const double* z, double* xn, void* stream) {
+    if (n < 0 || !ws_zz || !st || (n > 0 && (!z || !xn))) return QDOT_ERR_ARG;
+    const int g = grid_for(n > 0 ? n : 1, 4);
+    k_pm_div<<<g, T, 0, static_cast<cudaStream_t>(stream)>>>(n, ws_zz, st, z, xn);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "pm_div");
+}
+
+int qdot_b200_pm_check(int64_t n, const void* ws_zz, const void* ws_lam, double* st, const double* xn, double* x,
+                       void* rec, long long* counter, unsigned long long handle, void* stream) {
+    if (n < 0 || !ws_zz || !ws_lam || !st || !rec || !counter || (n > 0 && (!xn || !x))) return QDOT_ERR_ARG;
+    const int g = grid_for(n > 0 ? n : 1, 4);
+    k_pm_check<<<g, T, 0, static_cast<cudaStream_t>(stream)>>>(n, ws_zz, ws_lam, st, xn, x,
+                                                                static_cast<unsigned char*>(rec), counter,
+                                                                (cudaGraphConditionalHandle)handle);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "pm_check");
 }
 
 int qdot_b200_acg_check(const void* ws_a, const void* ws_b, const double* st, void* rec, long long* counter,

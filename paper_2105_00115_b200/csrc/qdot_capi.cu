@@ -6,6 +6,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <vector>
@@ -153,6 +154,49 @@ int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const
     return QDOT_OK;
 }
 
+// the one-launch cluster path (qdot_small.cuh): single device, exact strategy,
+// auto pass-1 mode, 1 <= n <= SMALL_AUTO (where it measured faster than the
+// four-launch pipeline: 12.7 vs 17.8 us per call at n = 1e4, APM n = 2000 61 vs
+// 67 us per iteration; at n = 32768 the ACG iteration was faster without it);
+// QDOT_B200_NO_SMALL=1 turns it off
+constexpr int64_t SMALL_AUTO = 16384;
+static bool small_ok(int64_t n, const qdot_config* cfg) {
+    static int off = -1;
+    if (off < 0) {
+        const char* e = std::getenv("QDOT_B200_NO_SMALL");
+        off = (e && e[0] && e[0] != '0') ? 1 : 0;
+    }
+    return !off && cfg && cfg->strategy == QDOT_STRATEGY_EXACT && cfg->reserved == 0 && n >= 1 &&
+           n <= (SMALL_AUTO < small_max() ? SMALL_AUTO : small_max());
+}
+
+int64_t qdot_b200_small_max(void) { return small_max(); }
+
+int qdot_b200_small(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                    void* stream) {
+    int v = validate(cfg);
+    if (v) return v;
+    if (!ws || n < 1 || n > small_max() || !x || (!norm && !y) || cfg->strategy != QDOT_STRATEGY_EXACT)
+        return QDOT_ERR_ARG;
+    WsPtrs w = ws_ptrs(ws);
+    QD_CHECK(launch_small(x, norm ? x : y, n, norm != 0, w.a, w.b, w.lut_bin, w.lut_p2, w.meta, w.result, w.bins, *cfg,
+                          static_cast<cudaStream_t>(stream)), "small");
+    return QDOT_OK;
+}
+
+int qdot_b200_enqueue(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                      void* stream) {
+    int r;
+    if (small_ok(n, cfg)) {
+        if ((r = qdot_b200_small(x, y, n, norm, cfg, ws, stream))) return r;
+    } else {
+        if ((r = qdot_b200_begin(ws, stream))) return r;
+        if ((r = qdot_b200_pass1(x, y, n, norm, cfg, n, ws, stream))) return r;
+    }
+    if ((r = qdot_b200_score_finalize(ws, n, cfg, stream))) return r;
+    return qdot_b200_pass2_finalize(x, y, n, norm, ws, stream);
+}
+
 static int score_impl(void* ws, int64_t n_total, const qdot_config* cfg, bool fuse, void* stream) {
     if (!ws || n_total < 0) return QDOT_ERR_ARG;
     int v = validate(cfg);
@@ -283,10 +327,7 @@ int enqueue_dot(const double* x, const double* y, int64_t n, int norm, const qdo
                 cudaStream_t st) {
     int r;
     void* s = static_cast<void*>(st);
-    if ((r = qdot_b200_begin(ws, s))) return r;
-    if ((r = qdot_b200_pass1(x, y, n, norm, cfg, n, ws, s))) return r;
-    if ((r = qdot_b200_score_finalize(ws, n, cfg, s))) return r;
-    if ((r = qdot_b200_pass2_finalize(x, y, n, norm, ws, s))) return r;
+    if ((r = qdot_b200_enqueue(x, y, n, norm, cfg, ws, s))) return r;
     FastState& F = g_fast;
     QD_CHECK(launch_publish(static_cast<const char*>(ws) + OFF_RESULT, PUBLISH_BYTES, F.host_dev, F.dev_seq,
                             reinterpret_cast<uint32_t*>(F.host_dev + PUBLISH_BYTES), st), "publish");

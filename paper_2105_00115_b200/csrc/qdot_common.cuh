@@ -86,6 +86,8 @@ constexpr int64_t A_HOT = 4224;         // [KEYS]: elements of the key accumulat
                                         // private window (exact HALF/SINGLE variants absent)
 constexpr int64_t A_PRIV = 8448;        // [KEYS]: elements of the key accumulated by any private
                                         // window (absent from the cold-element list)
+constexpr int64_t A_SMALL = 12664;      // k_small's outcome: 1 finished the call, 2 handed it to k_score
+                                        // (0 after begin: the multi-CTA pipeline)
 constexpr int64_t A_LEN = 12672;        // padded
 
 constexpr int64_t B_D0 = 0;             // DOUBLE limbs, weights 2^0, 2^32, 2^64, 2^96
@@ -327,6 +329,8 @@ QD_HD double ldexp_rn(double acc, int64_t u, int* overflow) {
     uint64_t b = dbits(acc);
     bool neg = b >> 63;
     int f = (int)((b >> 52) & 0x7FF);
+    if (f && u > -1022 && u < 1023 && f + (int)u > 0 && f + (int)u < 0x7FF)   // normal in, normal out: exact
+        return bitsd(b + ((uint64_t)(int64_t)u << 52));
     uint64_t m = b & ((1ull << 52) - 1);
     int q;
     if (f) { m |= 1ull << 52; q = f - 1075; } else { q = -1074; }

@@ -25,6 +25,7 @@
 // No tensor cores: this is a memory-bound integer/bit reduction.
 #include <cstdlib>
 
+#include <cooperative_groups.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -173,6 +174,24 @@ __device__ __forceinline__ double round_i128(__int128 v, int lsb, int mu, int em
     const bool neg = v < 0;
     unsigned __int128 a = neg ? (unsigned __int128)(-v) : (unsigned __int128)v;
     const uint64_t hi = (uint64_t)(a >> 64);
+    if (mu == 52 || mu == 23) {
+        // fast path: the hardware's round-to-nearest-even conversion of the leading
+        // 64 bits (the discarded bits OR-ed into bit 0 as sticky: >= 11 bits are
+        // dropped, so the round bit is kept), then an exact exponent shift when the
+        // result is a normal number strictly inside [emin, emax]
+        int sh = 0;
+        uint64_t top = (uint64_t)a;
+        if (hi) {
+            sh = 64 - clz64(hi);
+            top = (uint64_t)(a >> sh) | ((a & (((unsigned __int128)1 << sh) - 1)) != 0 ? 1ull : 0ull);
+        }
+        const double r = mu == 52 ? __ull2double_rn(top) : (double)__ull2float_rn(top);
+        const int er = (int)((dbits(r) >> 52) & 0x7FF) - 1023 + lsb + sh;
+        if (er > emin && er < emax) {
+            const double s = bitsd(dbits(r) + ((uint64_t)(int64_t)(lsb + sh) << 52));
+            return neg ? -s : s;
+        }
+    }
     if (!hi) return round_scaled((uint64_t)a, lsb, false, neg, mu, emin, emax, ovf);
     const int sh = 64 - clz64(hi);                 // bits above the low 64
     const uint64_t top = (uint64_t)(a >> sh);
@@ -281,12 +300,14 @@ __device__ double bin_value(const K& kk, const qdot_bin& bn, int* ovf, int* hf) 
 
 // qdot_accumulate: Neumaier over bins in ascending-upper order (emulate.py:55-72)
 __device__ __forceinline__ void neumaier_fold(const double* v, int cn, double& sum, double& c) {
+    // branch-free: the larger-magnitude operand is the one t is subtracted from
 #pragma unroll 4
     for (int i = 0; i < cn; ++i) {
         const double x = v[i];
         const double t = __dadd_rn(sum, x);
-        if (fabs(sum) >= fabs(x)) c = __dadd_rn(c, __dadd_rn(__dsub_rn(sum, t), x));
-        else c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), sum));
+        const bool ge = fabs(sum) >= fabs(x);
+        const double big = ge ? sum : x, small = ge ? x : sum;
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(big, t), small));
         sum = t;
     }
 }
@@ -304,27 +325,27 @@ __device__ __forceinline__ void block_count_reduce(const long long (&cnt_local)[
 // the result header (kernel.py:175, scoring.py:192-216) and the phase times
 __device__ void write_result(unsigned long long ts0, unsigned long long ts1, const ScoreMeta& m, double sum, double c,
                              const unsigned long long* s_cnt, int s_ovf, int s_half, qdot_result* __restrict__ res) {
-    qdot_result r;
-    memset(&r, 0, sizeof(r));
-    r.value = (sum - sum == 0.0) ? __dadd_rn(sum, c) : sum;
-    for (int i = 0; i < 4; ++i) r.counts[i] = (long long)s_cnt[i];
-    r.counts[QDOT_PERFORATE] += m.zero;                                        // kernel.py:175
-    r.eps_eff = m.eps_eff;
-    r.n = m.n_total;
-    r.nnz = m.nnz;
-    r.zero_count = m.zero;
-    r.status = m.status != QDOT_OK ? m.status : (s_ovf ? QDOT_ERR_OVERFLOW : QDOT_OK);
-    r.n_bins = m.n_bins;
-    r.e_min = m.e_min;
-    r.e_max = m.e_max;
-    r.early_terminated = m.early;
-    r.pass2_needed = m.need_p2;
-    r.half_order_sensitive = s_half;
+    // field by field (a local struct + memset would go through local memory)
+    qdot_result* r = res;
+    r->value = (sum - sum == 0.0) ? __dadd_rn(sum, c) : sum;
+    for (int i = 0; i < 4; ++i)
+        r->counts[i] = (long long)s_cnt[i] + (i == QDOT_PERFORATE ? m.zero : 0);   // kernel.py:175
+    r->eps_eff = m.eps_eff;
+    r->n = m.n_total;
+    r->nnz = m.nnz;
+    r->zero_count = m.zero;
+    r->status = m.status != QDOT_OK ? m.status : (s_ovf ? QDOT_ERR_OVERFLOW : QDOT_OK);
+    r->n_bins = m.n_bins;
+    r->e_min = m.e_min;
+    r->e_max = m.e_max;
+    r->early_terminated = m.early;
+    r->pass2_needed = m.need_p2;
+    r->half_order_sensitive = s_half;
     const unsigned long long now = global_ns();
     const unsigned long long sel = ts1 > ts0 ? ts1 - ts0 : 0ull, cmp = now > ts1 ? now - ts1 : 0ull;
-    r.select_ns = (int32_t)(sel < 0x7FFFFFFFull ? sel : 0x7FFFFFFFull);
-    r.compute_ns = (int32_t)(cmp < 0x7FFFFFFFull ? cmp : 0x7FFFFFFFull);
-    *res = r;
+    r->select_ns = (int32_t)(sel < 0x7FFFFFFFull ? sel : 0x7FFFFFFFull);
+    r->compute_ns = (int32_t)(cmp < 0x7FFFFFFFull ? cmp : 0x7FFFFFFFull);
+    r->reserved[0] = 0; r->reserved[1] = 0; r->reserved[2] = 0;
 }
 
 // per-bin values + Neumaier fold + result header from global memory; any
@@ -396,17 +417,31 @@ k_finalize(const int64_t* __restrict__ A, const int64_t* __restrict__ B, const u
 // =============================================================================
 constexpr int SW_KEYS = 64;
 
-__device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* __restrict__ lut_bin,
+// where score_warp reads the per-key totals: the global exchange regions (k_score) ...
+struct GlobalSrc {
+    const int64_t* __restrict__ A;
+    const int64_t* __restrict__ B;
+    const uint32_t* __restrict__ lut_p2;
+    __device__ __forceinline__ long long cnt(int k) const { return A[A_CNT + k]; }
+    __device__ __forceinline__ long long hot(int k) const { return A[A_HOT + k]; }
+    __device__ __forceinline__ long long priv(int k) const { return A[A_PRIV + k]; }
+    __device__ __forceinline__ GlobalKeys keys() const { return GlobalKeys{A, B, lut_p2}; }
+};
+
+template <class Src>
+__device__ int score_warp(const Src& src, const int64_t* __restrict__ A, int32_t* __restrict__ lut_bin,
                            uint32_t* __restrict__ lut_p2, ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res,
                            qdot_bin* __restrict__ bins, int64_t n_total, const qdot_config& cfg, int kmin, int kmax,
                            unsigned long long ts0, long long a_nonfinite, long long a_zero, long long a_listovf,
-                           double* sval, long long* bup, signed char* bprec) {
+                           double* sval, long long* bup, signed char* bprec, long long* dbg = nullptr) {
     const int lane = threadIdx.x & 31;
+    const long long dc0 = clock64();
+    auto mark = [&](int i) { if (dbg && lane == 0) dbg[i] = clock64() - dc0; };
     long long c[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int k = kmin + lane + 32 * h;
-        c[h] = (k <= kmax) ? A[A_CNT + k] : 0;
+        c[h] = (k <= kmax) ? src.cnt(k) : 0;
     }
     const unsigned long long P = (unsigned long long)__ballot_sync(0xffffffffu, c[0] != 0) |
                                  ((unsigned long long)__ballot_sync(0xffffffffu, c[1] != 0) << 32);
@@ -477,6 +512,7 @@ __device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restr
         S = (unsigned long long)__reduce_or_sync(0xffffffffu, nx[0]) |
             ((unsigned long long)__reduce_or_sync(0xffffffffu, nx[1]) << 32) | 1ull;
     }
+    mark(0);
     const int nb = __popcll(S);
     const double eps_eff = (cfg.split == 1 && nb) ? __ddiv_rn(cfg.epsilon, (double)nb) : cfg.epsilon;   // scoring.py:192
     bool okf = true;
@@ -535,6 +571,7 @@ __device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restr
         bprec[bidx[h]] = (signed char)ob[h].precision;
     }
     __syncwarp();
+    mark(1);
     // ---- LUTs over [kmin, kmax] (lane's keys): bin id, pass-2 descriptor
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -549,10 +586,10 @@ __device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restr
             const int pr = bprec[b];
             if ((pr == QDOT_HALF || pr == QDOT_SINGLE) && status == QDOT_OK) {
                 const long long delta = bup[b] - (long long)(k - KOFF);
-                if (delta > 0 || A[A_HOT + k] > 0) {
+                if (delta > 0 || src.hot(k) > 0) {
                     d = P2_NEED | (pr == QDOT_HALF ? P2_HALF : 0u) | (uint32_t)(delta > P2_DELTA_MAX ? P2_DELTA_MAX : delta);
                     need = 1;
-                    if (A[A_PRIV + k] > 0) priv = 1;
+                    if (src.priv(k) > 0) priv = 1;
                 }
             }
         }
@@ -569,12 +606,13 @@ __device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restr
     if (lane == 0) *meta = m;
     unsigned long long ts1 = 0;
     if (lane == 0) { ts1 = global_ns(); ws_stamps(A)[1] = ts1; }
-    if (need) return;                                                    // pass 2 finalizes
+    mark(2);
+    if (need) return need;                                               // pass 2 finalizes
     __syncwarp();
     // ---- bin values, precision counts, fold, header
     long long cnt_local[4] = {0, 0, 0, 0};
     int ovf = 0, half = 0;
-    const GlobalKeys kk{A, B, lut_p2};
+    const auto kk = src.keys();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         if (bidx[h] < 0 || status != QDOT_OK) continue;
@@ -588,6 +626,7 @@ __device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restr
 #pragma unroll
         for (int p = 0; p < 4; ++p) cnt_local[p] += ob[h].precision == p ? ob[h].cardinality : 0;
     }
+    mark(3);
     ovf = __reduce_or_sync(0xffffffffu, ovf);
     half = __reduce_or_sync(0xffffffffu, half);
     unsigned long long s_cnt[4];
@@ -601,8 +640,11 @@ __device__ void score_warp(const int64_t* __restrict__ A, const int64_t* __restr
     if (lane == 0) {
         double sum = 0.0, cc = 0.0;
         neumaier_fold(sval, status == QDOT_OK ? nb : 0, sum, cc);
+        mark(4);
         write_result(ts0, ts1, m, sum, cc, s_cnt, ovf, half, res);
+        mark(5);
     }
+    return 0;
 }
 // =============================================================================
 // score (one CTA)
@@ -616,6 +658,7 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
     const int tid = threadIdx.x;
     pdl_wait();
     pdl_trigger();
+    if (A[A_SMALL] == 1) return;          // k_small scored and finalized this call
     SC_STAMP(0);
 
     // the flag words are loaded up front so their latency overlaps the counts'
@@ -652,8 +695,8 @@ k_score(const int64_t* __restrict__ A, const int64_t* __restrict__ B, int32_t* _
             const long long z0 = __shfl_sync(0xffffffffu, a_zero, 0);
             const long long lo0 = __shfl_sync(0xffffffffu, a_listovf, 0);
             const unsigned long long t0 = __shfl_sync(0xffffffffu, ts0, 0);
-            score_warp(A, B, lut_bin, lut_p2, meta, res, bins, n_total, cfg, kmin, kmax, t0, nf0, z0, lo0, S.sval,
-                       S.bup, S.bprec);
+            score_warp(GlobalSrc{A, B, lut_p2}, A, lut_bin, lut_p2, meta, res, bins, n_total, cfg, kmin, kmax, t0, nf0,
+                       z0, lo0, S.sval, S.bup, S.bprec);
         }
         return;
     }
@@ -1050,6 +1093,7 @@ k_pass2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
 
 
 #include "qdot_batched.cuh"
+#include "qdot_small.cuh"
 
 // =============================================================================
 // bin ids (lazy Bin.indices)
@@ -1184,6 +1228,28 @@ cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, u
     kernel_occupancy(k_score, SC_T, smem, cache);   // per-device shared-memory opt-in
     return launch_pdl(k_score, 1, SC_T, smem, st, A, B, lut_bin, lut_p2, meta, res, bins, n_total, cfg, fuse ? 1 : 0);
 }
+
+cudaError_t launch_small(const double* x, const double* y, int64_t n, bool norm, int64_t* A, int64_t* B,
+                         int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta, qdot_result* res, qdot_bin* bins,
+                         const qdot_config& cfg, cudaStream_t st) {
+    const bool vec = ((reinterpret_cast<uintptr_t>(x) | (norm ? 0 : reinterpret_cast<uintptr_t>(y))) & 15u) == 0;
+    auto kern = norm ? (vec ? k_small<true, true> : k_small<true, false>)
+                     : (vec ? k_small<false, true> : k_small<false, false>);
+    static KernelDevCache cache[4];
+    const size_t smem = sizeof(SmShared);
+    // per-device shared-memory opt-in (the occupancy query itself is not needed)
+    const int d = current_device();
+    KernelDevCache& c = cache[(norm ? 2 : 0) + (vec ? 1 : 0)];
+    if (!c.occ[d]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        c.occ[d] = 1;
+    }
+    kern<<<SM_CL, SM_T, smem, st>>>(x, norm ? x : y, n, A, B, lut_bin, lut_p2, meta, res, bins, cfg);
+    return cudaGetLastError();
+}
+
+int64_t small_max() { return SM_MAX; }
 
 cudaError_t launch_begin(void* region, size_t bytes, cudaStream_t st) {
     const int64_t n16 = (int64_t)(bytes / 16);

@@ -26,6 +26,13 @@ struct P2Fin {
 cudaError_t launch_pass2(const double* x, const double* y, int64_t n, bool norm, const uint32_t* lut_p2,
                          const ScoreMeta* meta, int64_t* B, const double2* list, const uint32_t* list_fill,
                          const P2Fin& fin, cudaStream_t st);
+// a whole single-device qdot of n <= small_max() elements (exact strategy) in one
+// cluster launch (qdot_small.cuh); score / pass 2 launched after it return at once
+// unless it handed the call over (A[A_SMALL] == 2)
+cudaError_t launch_small(const double* x, const double* y, int64_t n, bool norm, int64_t* A, int64_t* B,
+                         int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta, qdot_result* res, qdot_bin* bins,
+                         const qdot_config& cfg, cudaStream_t st);
+int64_t small_max();
 // zero `bytes` (a multiple of 16, 16-byte aligned) at region: regions A, B, local
 cudaError_t launch_begin(void* region, size_t bytes, cudaStream_t st);
 cudaError_t launch_finalize(const int64_t* A, const int64_t* B, const uint32_t* lut_p2, const ScoreMeta* meta,

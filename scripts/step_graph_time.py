@@ -19,7 +19,13 @@ c = config_struct(Q.ToleranceConfig(1e-8), Q.ExactBinning())
 cr = ctypes.byref(c)
 
 
+PIPE = os.environ.get("PIPE", "enqueue")
+
+
 def step(s):
+    if PIPE == "enqueue":        # the product path (one cluster launch at small n)
+        lib.qdot_b200_enqueue(x.data_ptr(), y.data_ptr(), n, 0, cr, ws, s)
+        return
     lib.qdot_b200_begin(ws, s)
     lib.qdot_b200_pass1(x.data_ptr(), y.data_ptr(), n, 0, cr, n, ws, s)
     lib.qdot_b200_score_finalize(ws, n, cr, s)
@@ -54,5 +60,5 @@ with torch.cuda.stream(cs):
     e1.record(cs)
     torch.cuda.synchronize()
     graph = e0.elapsed_time(e1) / 400 * 1e3
-print(json.dumps({"n": n, "pdl": os.environ.get("QDOT_B200_PDL", "1"), "eager_us_per_step": eager,
+print(json.dumps({"n": n, "pipe": PIPE, "pdl": os.environ.get("QDOT_B200_PDL", "1"), "eager_us_per_step": eager,
                   "graph_us_per_step": graph}))
