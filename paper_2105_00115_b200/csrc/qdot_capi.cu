@@ -158,16 +158,19 @@ int qdot_b200_pass1(const double* x, const double* y, int64_t n, int norm, const
 // auto pass-1 mode, 1 <= n <= SMALL_AUTO (where it measured faster than the
 // four-launch pipeline: 12.7 vs 17.8 us per call at n = 1e4, APM n = 2000 61 vs
 // 67 us per iteration; at n = 32768 the ACG iteration was faster without it);
-// QDOT_B200_NO_SMALL=1 turns it off
+// QDOT_B200_NO_SMALL=1 turns it off, QDOT_B200_SMALL_AUTO=m moves the limit (experiments)
 constexpr int64_t SMALL_AUTO = 16384;
 static bool small_ok(int64_t n, const qdot_config* cfg) {
     static int off = -1;
+    static int64_t lim = 0;
     if (off < 0) {
         const char* e = std::getenv("QDOT_B200_NO_SMALL");
         off = (e && e[0] && e[0] != '0') ? 1 : 0;
+        const char* m = std::getenv("QDOT_B200_SMALL_AUTO");
+        lim = m ? std::atoll(m) : SMALL_AUTO;
+        if (lim > small_max()) lim = small_max();
     }
-    return !off && cfg && cfg->strategy == QDOT_STRATEGY_EXACT && cfg->reserved == 0 && n >= 1 &&
-           n <= (SMALL_AUTO < small_max() ? SMALL_AUTO : small_max());
+    return !off && cfg && cfg->strategy == QDOT_STRATEGY_EXACT && cfg->reserved == 0 && n >= 1 && n <= lim;
 }
 
 int64_t qdot_b200_small_max(void) { return small_max(); }

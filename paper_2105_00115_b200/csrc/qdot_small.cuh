@@ -56,7 +56,8 @@ struct __align__(16) SmShared {
     unsigned long long zc, nf;                   // zero / non-finite products of this CTA (CTA 0: cluster)
     int oor;                                     // an element this path cannot keep (hand over)
     int kmx;
-    int decision;                                // CTA 0: 1 finish here, 2 hand over
+    int decision;                                // CTA 0: 1 finish here, 2 hand over (read by every CTA)
+    int post;                                    // CTA 0: score_warp asked for a pass 2 (hand over after all)
     int kmin, kmax;
 };
 
@@ -169,6 +170,9 @@ k_small(const double* __restrict__ x, const double* __restrict__ y, int64_t n, i
     const int tid = threadIdx.x, lane = tid & 31;
     const unsigned long long ts0 = global_ns();
     pdl_trigger();                               // k_score may be scheduled; it waits for this grid
+    // split cluster barrier: every CTA has started (its shared memory exists)
+    // before any distributed-shared-memory access; the wait is just before the push
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     // phase clocks of CTA 0 (SM cycles since entry) in A[A_SMALL + 1 ..]: diagnostics
     const long long c0 = clock64();
     auto phase = [&](int i) {
@@ -183,7 +187,7 @@ k_small(const double* __restrict__ x, const double* __restrict__ y, int64_t n, i
     // ---- clear, and the common sample: elements [0, 2 SM_T) -> largest key
     for (int i = tid; i < P1_W * SM_T; i += SM_T) S.priv[i] = make_ulonglong2(0ull, 0ull);
     for (int i = tid; i < 8 * SM_K; i += SM_T) (&S.c[0][0])[i] = 0u;
-    if (tid == 0) { S.zc = 0; S.nf = 0; S.oor = 0; S.kmx = -1; S.decision = 0; }
+    if (tid == 0) { S.zc = 0; S.nf = 0; S.oor = 0; S.kmx = -1; S.decision = 0; S.post = 0; }
     __syncthreads();
     {
         double xv[2], yv[2];
@@ -304,6 +308,7 @@ k_small(const double* __restrict__ x, const double* __restrict__ y, int64_t n, i
     // no round trips), CTA 0 sums them and decides
     __syncthreads();
     phase(3);
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     {
         SmShared* R0 = cl.map_shared_rank(&S, 0);
         if (tid < SM_K) {
@@ -359,10 +364,10 @@ k_small(const double* __restrict__ x, const double* __restrict__ y, int64_t n, i
                 const int need = score_warp(SmallSrc{&S, cbase}, A, lut_bin, lut_p2, meta, res, bins, n, cfg, S.kmin,
                                             S.kmax, ts0, (long long)S.nf, (long long)S.zc, 0ll, S.sval, S.bup,
                                             S.bprec);
-                if (lane == 0) S.decision = need ? 3 : 1;              // a pass 2 reads the global regions
+                if (lane == 0) S.post = need;                        // a pass 2 reads the global regions
             }
             __syncthreads();
-            if (S.decision == 3) {
+            if (S.post) {
                 // (early termination below input_mu 52: HALF / SINGLE products of keys under
                 // the bin's upper) -- hand the totals to k_score / k_pass2 through regions A / B
                 ulonglong2* z = reinterpret_cast<ulonglong2*>(A);
