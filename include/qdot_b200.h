@@ -154,7 +154,7 @@ int qdot_b200_enqueue(const double* x, const double* y, int64_t n, int norm, con
                       void* stream);
 int qdot_b200_small(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
                     void* stream);
-int64_t qdot_b200_small_max(void);   /* qdot_b200_small's limit (65536) */
+int64_t qdot_b200_small_max(void);   /* qdot_b200_small's limit (131072) */
 /* one-CTA scoring on the (reduced) histogram: partition, scores, precisions.
  * Replaces kernel.select_parameters' partition + scoring (kernel.py:59-72,
  * binning.py:191-284, scoring.py:126-216).  n_total = elements over all ranks. */

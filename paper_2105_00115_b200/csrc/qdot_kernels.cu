@@ -1229,24 +1229,45 @@ cudaError_t launch_score(const int64_t* A, const int64_t* B, int32_t* lut_bin, u
     return launch_pdl(k_score, 1, SC_T, smem, st, A, B, lut_bin, lut_p2, meta, res, bins, n_total, cfg, fuse ? 1 : 0);
 }
 
+template <int CL>
+static cudaError_t launch_small_cl(const double* x, const double* y, int64_t n, bool norm, int64_t* A, int64_t* B,
+                                   int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta, qdot_result* res,
+                                   qdot_bin* bins, const qdot_config& cfg, cudaStream_t st, bool vec) {
+    auto kern = norm ? (vec ? k_small<true, true, CL> : k_small<true, false, CL>)
+                     : (vec ? k_small<false, true, CL> : k_small<false, false, CL>);
+    static KernelDevCache cache[4];
+    const size_t smem = sizeof(SmShared);
+    const int d = current_device();
+    KernelDevCache& c = cache[(norm ? 2 : 0) + (vec ? 1 : 0)];
+    if (!c.occ[d]) {        // per-device attributes: shared-memory opt-in, 16-CTA clusters
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess && CL > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        c.occ[d] = 1;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(CL);
+    lc.blockDim = dim3(SM_T);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, kern, x, norm ? x : y, n, A, B, lut_bin, lut_p2, meta, res, bins, cfg);
+}
+
 cudaError_t launch_small(const double* x, const double* y, int64_t n, bool norm, int64_t* A, int64_t* B,
                          int32_t* lut_bin, uint32_t* lut_p2, ScoreMeta* meta, qdot_result* res, qdot_bin* bins,
                          const qdot_config& cfg, cudaStream_t st) {
     const bool vec = ((reinterpret_cast<uintptr_t>(x) | (norm ? 0 : reinterpret_cast<uintptr_t>(y))) & 15u) == 0;
-    auto kern = norm ? (vec ? k_small<true, true> : k_small<true, false>)
-                     : (vec ? k_small<false, true> : k_small<false, false>);
-    static KernelDevCache cache[4];
-    const size_t smem = sizeof(SmShared);
-    // per-device shared-memory opt-in (the occupancy query itself is not needed)
-    const int d = current_device();
-    KernelDevCache& c = cache[(norm ? 2 : 0) + (vec ? 1 : 0)];
-    if (!c.occ[d]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        c.occ[d] = 1;
-    }
-    kern<<<SM_CL, SM_T, smem, st>>>(x, norm ? x : y, n, A, B, lut_bin, lut_p2, meta, res, bins, cfg);
-    return cudaGetLastError();
+    // the portable 8-CTA cluster up to SM_CL_SPLIT elements, 16 CTAs above
+    return n <= SM_CL_SPLIT
+        ? launch_small_cl<SM_CL_SMALL>(x, y, n, norm, A, B, lut_bin, lut_p2, meta, res, bins, cfg, st, vec)
+        : launch_small_cl<SM_CL>(x, y, n, norm, A, B, lut_bin, lut_p2, meta, res, bins, cfg, st, vec);
 }
 
 int64_t small_max() { return SM_MAX; }

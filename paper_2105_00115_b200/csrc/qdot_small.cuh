@@ -3,7 +3,7 @@
 //
 // The multi-CTA pipeline (begin, pass 1, score, pass 2) costs four dependent
 // launches and a 400 KB workspace reset -- at the solvers' sizes (n ~ 1e3 ..
-// 6e4, apps.py:178-229, 275-325) that is the whole call.  Here the SM_CL CTAs
+// 6e4, apps.py:178-229, 275-325) that is the whole call.  Here the CL CTAs
 // of one cluster keep every exact per-key partial in shared memory:
 //
 //   1. window: each CTA reads the same first 2 SM_T elements (its own first
@@ -31,11 +31,13 @@
 
 // (cooperative_groups.h is included at the top of qdot_kernels.cu, outside namespace qd)
 
-constexpr int SM_CL = 8;                         // CTAs per cluster (portable size)
+constexpr int SM_CL = 16;                        // CTAs per cluster, at most (16: non-portable, B200 runs it)
+constexpr int SM_CL_SMALL = 8;                   // n <= SM_CL_SPLIT: the portable 8
 constexpr int SM_T = 256;                        // threads per CTA
 constexpr int SM_K = 64;                         // table keys (= score_warp's span)
 constexpr int SM_EPT = 32;                       // elements per thread at the size limit (<= 255: slot count)
-constexpr int64_t SM_MAX = (int64_t)SM_CL * SM_T * SM_EPT;   // 65536
+constexpr int64_t SM_MAX = (int64_t)SM_CL * SM_T * SM_EPT;   // 131072
+constexpr int64_t SM_CL_SPLIT = 16384;
 static_assert(SM_K == SW_KEYS, "score_warp scores the table");
 
 struct __align__(16) SmShared {
@@ -157,8 +159,9 @@ __device__ __forceinline__ void sm_load2(const double* __restrict__ x, const dou
     }
 }
 
-template <bool NORM, bool VEC>
-__global__ void __cluster_dims__(SM_CL, 1, 1) __launch_bounds__(SM_T, 1)
+// CL CTAs per cluster (launched with a cluster-dimension attribute)
+template <bool NORM, bool VEC, int CL>
+__global__ void __launch_bounds__(SM_T, 1)
 k_small(const double* __restrict__ x, const double* __restrict__ y, int64_t n, int64_t* __restrict__ A,
         int64_t* __restrict__ B, int32_t* __restrict__ lut_bin, uint32_t* __restrict__ lut_p2,
         ScoreMeta* __restrict__ meta, qdot_result* __restrict__ res, qdot_bin* __restrict__ bins, qdot_config cfg) {
@@ -179,7 +182,7 @@ k_small(const double* __restrict__ x, const double* __restrict__ y, int64_t n, i
         if (rank == 0 && tid == 0) A[A_SMALL + i] = clock64() - c0;
     };
 
-    const int64_t stride = 2 * (int64_t)SM_T * SM_CL;
+    const int64_t stride = 2 * (int64_t)SM_T * CL;
     const int64_t i0 = 2 * ((int64_t)rank * SM_T + tid);
     double cx[2] = {0.0, 0.0}, cy[2] = {0.0, 0.0};          // this thread's first pair, in flight
     bool cok[2] = {false, false};                           // during the sample's reduction
@@ -331,13 +334,13 @@ k_small(const double* __restrict__ x, const double* __restrict__ y, int64_t n, i
             long long a = 0, h = 0;
             unsigned long long c = 0;
 #pragma unroll
-            for (int q = 0; q < SM_CL; ++q) { d += S.rd[q][j]; a += S.rs[q][j]; h += S.rh[q][j]; c += S.rc[q][j]; }
+            for (int q = 0; q < CL; ++q) { d += S.rd[q][j]; a += S.rs[q][j]; h += S.rh[q][j]; c += S.rc[q][j]; }
             S.td[j] = d; S.tsum[j] = a; S.thalf[j] = h; S.tcnt[j] = c;
         } else if (tid == SM_K) {
             unsigned long long z = 0, f = 0;
             int o = 0;
 #pragma unroll
-            for (int q = 0; q < SM_CL; ++q) { z += S.rzc[q]; f += S.rnf[q]; o |= S.roor[q]; }
+            for (int q = 0; q < CL; ++q) { z += S.rzc[q]; f += S.rnf[q]; o |= S.roor[q]; }
             S.zc = z; S.nf = f; S.oor = o;
         }
         __syncthreads();
@@ -391,7 +394,7 @@ k_small(const double* __restrict__ x, const double* __restrict__ y, int64_t n, i
         // ---- hand over: zero the exchange regions, add what this path kept, push the rest
         ulonglong2* z = reinterpret_cast<ulonglong2*>(A);     // regions A, B, local are contiguous
         const int64_t n16 = (BYTES_A + BYTES_B + BYTES_LOCAL) / 16;
-        for (int64_t i = (int64_t)rank * SM_T + tid; i < n16; i += (int64_t)SM_CL * SM_T)
+        for (int64_t i = (int64_t)rank * SM_T + tid; i < n16; i += (int64_t)CL * SM_T)
             z[i] = make_ulonglong2(0ull, 0ull);
         __threadfence();
         cl.sync();
