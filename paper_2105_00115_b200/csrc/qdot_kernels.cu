@@ -35,6 +35,16 @@
 namespace qd {
 
 #include "qdot_pass1.cuh"
+// norm mode's pass 1: the same code with 11 private slots, four CTAs per SM
+namespace p1n {
+#undef QDOT_P1_W
+#undef QDOT_P1_WW
+#undef QDOT_P1_MINB
+#define QDOT_P1_W 11
+#define QDOT_P1_WW 17
+#define QDOT_P1_MINB 4
+#include "qdot_pass1.cuh"
+}  // namespace p1n
 
 // phase clocks of the score/finalize CTA (scripts/score_prof.cu builds with it)
 #ifdef QDOT_SCORE_PROFILE
@@ -1155,13 +1165,19 @@ __global__ void __launch_bounds__(256) k_begin(ulonglong2* __restrict__ p, int64
 
 static int sm_count_cached() { return device_sm_count(); }
 
-template <bool NORM, bool VEC, int V, bool PF, int L2D, bool SMALL = false>
+// NARROW: the 11-slot build (namespace p1n; norm mode)
+template <bool NORM, bool VEC, int V, bool PF, int L2D, bool SMALL = false, bool NARROW = false>
 static cudaError_t launch_pass1_t(const double* x, const double* y, int64_t n, int64_t* A, int64_t* B,
                                   const P1Params& prm, cudaStream_t st) {
-    auto kern = k_pass1<NORM, VEC, V, PF, L2D, SMALL>;
-    const size_t smem = sizeof(P1Shared);
+    auto kern = NARROW ? p1n::k_pass1<NORM, VEC, V, PF, L2D, SMALL> : k_pass1<NORM, VEC, V, PF, L2D, SMALL>;
+    const size_t smem = NARROW ? sizeof(p1n::P1Shared) : sizeof(P1Shared);
     static KernelDevCache cache;
-    const int occ = kernel_occupancy(kern, P1_T, smem, cache);
+    int occ = kernel_occupancy(kern, P1_T, smem, cache);
+    {   // QDOT_B200_P1_OCC=k: at most k CTAs per SM in the grid (occupancy experiments)
+        static int cap = -1;
+        if (cap < 0) { const char* e = getenv("QDOT_B200_P1_OCC"); cap = e ? atoi(e) : 0; }
+        if (cap > 0 && cap < occ) occ = cap;
+    }
     const int64_t tile = (int64_t)P1_T * 2 * V;
     int64_t ntiles = (n + tile - 1) / tile;
     int64_t grid = (int64_t)sm_count_cached() * occ;
@@ -1207,6 +1223,11 @@ static cudaError_t launch_pass1_v(const double* x, const double* y, int64_t n, i
 #endif
     // V = 4 double2 per thread per tile, bulk L2 prefetch 4 tiles ahead: tuned on
     // B200 (norm mode: V = 8 measured slower)
+    if (NORM) {   // norm mode: the 11-slot build, four CTAs per SM (QDOT_B200_P1_NARROW=0: the 16-slot one)
+        static int narrow = -1;
+        if (narrow < 0) { const char* e = getenv("QDOT_B200_P1_NARROW"); narrow = (e && e[0] == '0') ? 0 : 1; }
+        if (narrow) return launch_pass1_t<NORM, VEC, 4, false, 3, false, true>(x, y, n, A, B, prm, st);
+    }
     return launch_pass1_t<NORM, VEC, 4, false, 3>(x, y, n, A, B, prm, st);
 }
 

@@ -28,9 +28,25 @@
 // The score kernel sends flagged keys that did become HALF/SINGLE to pass 2,
 // so the prediction only affects speed, never results.
 
+// The file is included twice (qdot_kernels.cu): with the defaults below for
+// x . y, and inside namespace p1n with QDOT_P1_W 11 / QDOT_P1_WW 17 /
+// QDOT_P1_MINB 4 for norm mode -- 11 private slots per thread instead of 16
+// fit four CTAs per SM instead of three (norm mode is latency-bound, x . y
+// HBM-bound).
+#ifndef QDOT_P1_W
+#define QDOT_P1_W 16
+#endif
+#ifndef QDOT_P1_WW
+#define QDOT_P1_WW 24
+#endif
+#ifndef QDOT_P1_MINB
+#define QDOT_P1_MINB 3
+#endif
 constexpr int P1_T = 256;                    // threads per CTA
-constexpr int P1_W = 16;                     // keys with per-thread private slots
-constexpr int P1_WW = 24;                    // wide lean window: {D int64, count u16} per (key, thread)
+constexpr int P1_W = QDOT_P1_W;              // keys with per-thread private slots
+constexpr int P1_WW = QDOT_P1_WW;            // wide lean window: {D int64, count u16} per (key, thread)
+static_assert(P1_WW * P1_T * 10 <= P1_W * P1_T * 16, "wide layout fits the private slots");
+static_assert(4224 * 8 + 4224 * 2 <= P1_W * P1_T * 16, "sampling scratch fits the private slots");
 constexpr int P1_CW = 128;                   // keys with per-CTA 32-bit limb tables
 // private window keys keep e in [-971, 1021]: fl(x*y) normal and finite and
 // 2^(52-e) representable
@@ -478,6 +494,39 @@ __device__ __forceinline__ void p1_prefetch_norm(const double* x, int64_t n, int
                  "r"(TILE * 8), "l"(pol) : "memory");
 }
 
+// WIDE: P1_WW exponents in the wide layout (int64 D at slot * P1_T * 8 + tid * 8,
+// u16 count after all D words) -- more exponents in the same bytes, for CTAs
+// whose sampled exponents spread beyond the P1_W-slot window (mys: the D base,
+// mysc: the count base of this thread)
+template <int V, bool FULLT>
+__device__ __forceinline__ uint32_t p1_tile_norm_wide(uint32_t mys, uint32_t mysc, uint32_t ebase,
+                                                      const double (&xv)[2 * V], int64_t e0, int64_t n, int tid) {
+    uint32_t cold = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * V; ++j) {
+        const uint32_t hi = (uint32_t)__double2hiint(xv[j]);
+        const uint32_t d = (hi & 0x7FF00000u) - ebase;
+        const bool ok = FULLT || e0 + 2 * ((int64_t)(j >> 1) * P1_T + tid) + (j & 1) < n;
+        uint32_t mh;
+        asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(mh) : "r"(hi), "r"(0x000FFFFFu), "r"(0x41900000u));
+        const double m26 = __hiloint2double((int)mh, __double2loint(xv[j]));
+        const long long kd = __double2ll_rn(__dmul_rn(m26, m26));
+        const bool hot = d < ((uint32_t)P1_WW << 20);
+        const uint32_t r = min(d, ((uint32_t)P1_WW - 1u) << 20) >> 20;
+        asm volatile("{\n\t.reg .pred p;\n\t.reg .u64 a;\n\t.reg .u16 c;\n\t"
+                     "setp.ne.u32 p, %3, 0;\n\t"
+                     "ld.shared.u64 a, [%0];\n\t"
+                     "add.s64 a, a, %2;\n\t"
+                     "@p st.shared.u64 [%0], a;\n\t"
+                     "ld.shared.u16 c, [%1];\n\t"
+                     "add.u16 c, c, 1;\n\t"
+                     "@p st.shared.u16 [%1], c;\n\t}"
+                     :: "r"(mys + r * (P1_T * 8)), "r"(mysc + r * (P1_T * 2)), "l"(kd), "r"((uint32_t)(hot && ok)));
+        if (!hot && ok) cold |= 1u << j;
+    }
+    return cold;
+}
+
 template <int V, bool FULLT>
 __device__ __forceinline__ uint32_t p1_tile_norm(uint32_t mys, uint32_t ebase, const double (&xv)[2 * V],
                                                  int64_t e0, int64_t n, int tid) {
@@ -494,7 +543,7 @@ __device__ __forceinline__ uint32_t p1_tile_norm(uint32_t mys, uint32_t ebase, c
         const bool hot = d < ((uint32_t)P1_W << 20);
         // slot {D lo, D hi, count, 0} at mys + slot * P1_T * 16 bytes.  Straight-line code
         // (no per-element branch / reconvergence): every element loads a slot (a cold one
-        // reads slot (d mod P1_W), harmlessly) and only a window element stores it back
+        // reads slot min(d, P1_W - 1), harmlessly) and only a window element stores it back
         asm volatile("{\n\t.reg .pred p;\n\t.reg .u32 a, b, c, w;\n\t"
                      "setp.ne.u32 p, %3, 0;\n\t"
                      "ld.shared.v4.u32 {a, b, c, w}, [%0];\n\t"
@@ -502,7 +551,7 @@ __device__ __forceinline__ uint32_t p1_tile_norm(uint32_t mys, uint32_t ebase, c
                      "addc.u32 b, b, %2;\n\t"
                      "add.u32 c, c, 1;\n\t"
                      "@p st.shared.v4.u32 [%0], {a, b, c, w};\n\t}"
-                     :: "r"(mys + ((d & (((uint32_t)P1_W - 1u) << 20)) >> 8)), "r"((uint32_t)kd),
+                     :: "r"(mys + (min(d, ((uint32_t)P1_W - 1u) << 20) >> 8)), "r"((uint32_t)kd),
                         "r"((uint32_t)((unsigned long long)kd >> 32)), "r"((uint32_t)(hot && ok)));
         // (no memory clobber: it would force the tile's registers into local memory; the
         // slots are touched by C++ code only across __syncthreads, and volatile asm keeps
@@ -514,16 +563,19 @@ __device__ __forceinline__ uint32_t p1_tile_norm(uint32_t mys, uint32_t ebase, c
 
 // one norm tile: window elements into the private slots, cold ones through the
 // warp queue, the flush every FLUSH tiles
-template <int V>
+template <int V, bool WIDE>
 __device__ __forceinline__ void p1_norm_tile(P1Shared& S, int64_t* __restrict__ A, int64_t* __restrict__ B,
-                                             uint32_t mys, uint32_t ebase, const double (&xv)[2 * V], int64_t t,
-                                             bool f, int64_t n, int tid, uint32_t& qn, int& since, uint32_t* zc,
-                                             uint32_t* nf) {
+                                             uint32_t mys, uint32_t mysc, uint32_t ebase, const double (&xv)[2 * V],
+                                             int64_t t, bool f, int64_t n, int tid, uint32_t& qn, int& since,
+                                             uint32_t* zc, uint32_t* nf) {
     constexpr int EPT = 2 * V;
     constexpr int FLUSH = 511 / EPT;                   // D < 511 * 2^54 per slot between flushes
     const int warp = tid >> 5, lane = tid & 31;
-    const uint32_t cold = f ? p1_tile_norm<V, true>(mys, ebase, xv, t * (P1_T * EPT), n, tid)
-                            : p1_tile_norm<V, false>(mys, ebase, xv, t * (P1_T * EPT), n, tid);
+    uint32_t cold;
+    if (WIDE) cold = f ? p1_tile_norm_wide<V, true>(mys, mysc, ebase, xv, t * (P1_T * EPT), n, tid)
+                       : p1_tile_norm_wide<V, false>(mys, mysc, ebase, xv, t * (P1_T * EPT), n, tid);
+    else cold = f ? p1_tile_norm<V, true>(mys, ebase, xv, t * (P1_T * EPT), n, tid)
+                  : p1_tile_norm<V, false>(mys, ebase, xv, t * (P1_T * EPT), n, tid);
     const uint32_t wm = __reduce_or_sync(0xffffffffu, cold);     // positions with a cold element in the warp
     if (wm) {
 #pragma unroll
@@ -532,7 +584,7 @@ __device__ __forceinline__ void p1_norm_tile(P1Shared& S, int64_t* __restrict__ 
     }
     if (++since == FLUSH) {
         p1_drain(S, A, B, warp, lane, qn, zc, nf);
-        p1_flush<false, P1_W>(S, A, B, tid);
+        p1_flush<false, WIDE ? P1_WW : P1_W>(S, A, B, tid);
         since = 0;
     }
 }
@@ -540,7 +592,7 @@ __device__ __forceinline__ void p1_norm_tile(P1Shared& S, int64_t* __restrict__ 
 // (register double buffering -- the next tile's loads issued before the current
 // tile is accumulated -- and two tiles per iteration both measured slower:
 // 0.60 / 0.49 vs 0.45 ms at 2^28, profiles/r2_norm_experiments.md)
-template <bool VEC, int V>
+template <bool VEC, int V, bool WIDE>
 __device__ __forceinline__ void p1_main_norm(P1Shared& S, const double* __restrict__ x, int64_t n,
                                              int64_t* __restrict__ A, int64_t* __restrict__ B, int tid,
                                              uint32_t* zc, uint32_t* nf, int L2D, int pmode) {
@@ -550,7 +602,9 @@ __device__ __forceinline__ void p1_main_norm(P1Shared& S, const double* __restri
     const int64_t stride = gridDim.x;
     // slot r holds key base + 2r, i.e. biased exponent fx = r + (base - KOFF) / 2 + 1023
     const uint32_t ebase = (uint32_t)((S.base - KOFF) / 2 + 1023) << 20;
-    const uint32_t mys = (uint32_t)__cvta_generic_to_shared(S.priv + tid);
+    const uint32_t pbase = (uint32_t)__cvta_generic_to_shared(S.priv);
+    const uint32_t mys = WIDE ? pbase + tid * 8 : pbase + tid * 16;
+    const uint32_t mysc = pbase + P1_WW * P1_T * 8 + tid * 2;      // wide layout's u16 counts
     int since = 0;
     uint32_t qn = 0;
     // prefetched lines: evict-first (0), evict-normal (1) or evict-last (2); the demand
@@ -569,18 +623,18 @@ __device__ __forceinline__ void p1_main_norm(P1Shared& S, const double* __restri
         bool f;
         if (L2D > 0 && tid == 0) p1_prefetch_norm(x, n, t + (L2D + 1) * stride, TILE, pol);
         p1_load<true, VEC, V>(x, x, n, t, tid, xv, yv, f);
-        p1_norm_tile<V>(S, A, B, mys, ebase, xv, t, f, n, tid, qn, since, zc, nf);
+        p1_norm_tile<V, WIDE>(S, A, B, mys, mysc, ebase, xv, t, f, n, tid, qn, since, zc, nf);
     }
     const int warp = tid >> 5, lane = tid & 31;
     p1_drain(S, A, B, warp, lane, qn, zc, nf);
-    p1_flush<false, P1_W>(S, A, B, tid);
+    p1_flush<false, WIDE ? P1_WW : P1_W>(S, A, B, tid);
 }
 
 // SMALL: the variant for short inputs (a few tiles per CTA), where the fixed
 // per-CTA cost dominates: one main loop (full variants, no queue, no L2
 // prefetch) keeps the code a CTA must fetch small.
 template <bool NORM, bool VEC, int V, bool PF, int L2D, bool SMALL>
-__global__ void __launch_bounds__(P1_T, 3)
+__global__ void __launch_bounds__(P1_T, QDOT_P1_MINB)
 k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         int64_t* __restrict__ A, int64_t* __restrict__ B, P1Params prm) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -787,7 +841,7 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
             // number of sampled keys under per-bin splitting (n_bins >= that number).
             constexpr int PER = (KEYS + P1_T - 1) / P1_T;
             constexpr int SPAN = 2 * P1_W - 1;
-            uint32_t* upref = hist + 8448;                                  // KEYS+1 u32
+            uint16_t* upref = reinterpret_cast<uint16_t*>(hist + 8448);    // KEYS+1 u16 (<= 2048)
             const int lane = tid & 31, warp = tid >> 5;
             const uint32_t ns = pref[KEYS];
             uint32_t nk = 0;
@@ -833,42 +887,59 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
             __syncthreads();
             uint32_t pre = incl - run;
             for (int w = 0; w < warp; ++w) pre += (uint32_t)S.red[w];
-            if (tid == 0) upref[0] = 0u;
+            if (tid == 0) upref[0] = 0;
 #pragma unroll
             for (int i = 0; i < PER; ++i) {
                 const int k = tid * PER + i;
-                if (k < KEYS) upref[k + 1] = pre + loc[i];
+                if (k < KEYS) upref[k + 1] = (uint16_t)(pre + loc[i]);
             }
             __syncthreads();
-            unsigned long long best = 0ull;
+            // best lean-safe window of P1_W exponents (16-byte slots) and of P1_WW
+            // exponents (the wide 10-byte layout)
+            constexpr int SPANW = 2 * P1_WW - 1;
+            unsigned long long best = 0ull, bestw = 0ull;
             const int lo = P1_SAFE_LO + ((P1_SAFE_LO - KOFF) & 1);           // keys of x . x have KOFF's parity
             for (int b = lo + 2 * tid; b + SPAN - 1 <= KOFF + 1021; b += 2 * P1_T) {
                 if (upref[b + SPAN] != upref[b]) continue;
                 const uint32_t cov = pref[b + SPAN] - pref[b];
                 const unsigned long long cand = ((unsigned long long)cov << 32) | (uint32_t)b;   // ties: larger b
                 best = cand > best ? cand : best;
+                if (b + SPANW - 1 <= KOFF + 1021 && upref[b + SPANW] == upref[b]) {
+                    const uint32_t cw = pref[b + SPANW] - pref[b];
+                    const unsigned long long cd = ((unsigned long long)cw << 32) | (uint32_t)b;
+                    bestw = cd > bestw ? cd : bestw;
+                }
             }
             for (int o = 16; o; o >>= 1) {
-                const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+                unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
                 best = t > best ? t : best;
+                t = __shfl_xor_sync(0xffffffffu, bestw, o);
+                bestw = t > bestw ? t : bestw;
             }
             __syncthreads();
-            if (lane == 0) S.red[warp] = best;
+            if (lane == 0) { S.red[warp] = best; S.red[P1_T / 32 + warp] = bestw; }
             __syncthreads();
             if (tid == 0) {
-                unsigned long long m = 0ull;
-                for (int w = 0; w < P1_T / 32; ++w) m = S.red[w] > m ? S.red[w] : m;
-                const uint32_t cov = (uint32_t)(m >> 32);
-                // worth it when the window holds >= 7/8 of the sample (the rest goes
-                // through the cold-element queue)
-                if (ns && (uint64_t)cov * 8u >= (uint64_t)ns * 7u) {
-                    const int b = (int)(uint32_t)m;
+                unsigned long long m = 0ull, mw = 0ull;
+                for (int w = 0; w < P1_T / 32; ++w) {
+                    m = S.red[w] > m ? S.red[w] : m;
+                    mw = S.red[P1_T / 32 + w] > mw ? S.red[P1_T / 32 + w] : mw;
+                }
+                const uint32_t cov = (uint32_t)(m >> 32), covw = (uint32_t)(mw >> 32);
+                // the 16-byte slots when they hold >= 99% of the sample, else the wide
+                // layout when it holds >= 7/8 (the rest goes through the cold-element queue)
+                int b = -1, wide = 0;
+                if (ns && (uint64_t)cov * 100u >= (uint64_t)ns * 99u) b = (int)(uint32_t)m;
+                else if (ns && covw > cov && (uint64_t)covw * 8u >= (uint64_t)ns * 7u) { b = (int)(uint32_t)mw; wide = 1; }
+                else if (ns && (uint64_t)cov * 8u >= (uint64_t)ns * 7u) b = (int)(uint32_t)m;
+                if (b >= 0) {
+                    const int span = wide ? SPANW : SPAN;
                     S.norm_lean = 1;
                     S.full = 0;
-                    S.wide = 0;
+                    S.wide = wide;
                     S.queue = 1;
                     S.base = b;
-                    int cb = b - (P1_CW - SPAN) / 2;
+                    int cb = b - (P1_CW - span) / 2;
                     cb = cb < 0 ? 0 : cb;
                     S.cbase = cb + P1_CW > KEYS ? KEYS - P1_CW : cb;
                 }
@@ -895,7 +966,8 @@ k_pass1(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
         // mode bits 6-7 select it for tuning: 0 -> L2D, 1 -> 2 L2D + 1, 2 -> none, 3 -> 1
         const int sel = (prm.mode >> 6) & 3;
         const int l2d = L2D == 0 ? 0 : (sel == 0 ? L2D : (sel == 1 ? 2 * L2D + 1 : (sel == 2 ? 0 : 1)));
-        p1_main_norm<VEC, V>(S, x, n, A, B, tid, &zc, &nf, l2d, (prm.mode >> 8) & 3);
+        if (S.wide) p1_main_norm<VEC, V, true>(S, x, n, A, B, tid, &zc, &nf, l2d, (prm.mode >> 8) & 3);
+        else p1_main_norm<VEC, V, false>(S, x, n, A, B, tid, &zc, &nf, l2d, (prm.mode >> 8) & 3);
     } else if (S.wide) {
         if (S.queue) p1_main<NORM, VEC, false, true, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
         else p1_main<NORM, VEC, false, false, V, PF, L2D, P1_WW>(S, x, y, n, A, B, tid, &zc, &nf);
