@@ -375,6 +375,8 @@ double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow);
  * shift = 0: abs_bound; e_max: rel_bound; reference.flexp_e: rel_bound_e.
  * QDOT_ERR_OVERFLOW where the reference raises OverflowError. */
 int qdot_b200_bound_sums(const qdot_bin* bins, int32_t n_bins, int64_t shift, double* out);
+/* both at once for shifts a then b (out[0..1], out[2..3]); the first failure is returned */
+int qdot_b200_bound_sums2(const qdot_bin* bins, int32_t n_bins, int64_t shift_a, int64_t shift_b, double* out);
 
 #ifdef __cplusplus
 }

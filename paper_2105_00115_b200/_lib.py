@@ -99,6 +99,7 @@ SIGNATURES = {
     "qdot_b200_batched_bins": (_I, [_P, _P, _I64, _I64, _I64, _I, ctypes.POINTER(QdotConfig), _P, _P, _P, _P, _P]),
     "qdot_b200_ldexp_rn": (ctypes.c_double, [ctypes.c_double, _I64, ctypes.POINTER(_I)]),
     "qdot_b200_bound_sums": (_I, [_P, ctypes.c_int32, _I64, _P]),
+    "qdot_b200_bound_sums2": (_I, [_P, ctypes.c_int32, _I64, _I64, _P]),
     "qdot_b200_csr_spmv": (_I, [_I64, _P, _P, _I, _P, _P, _P, _P]),
     "qdot_b200_read_probe": (_I, [_P, _I64, _P, _P]),
     "qdot_b200_sell_spmv": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P]),

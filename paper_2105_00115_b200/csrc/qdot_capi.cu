@@ -552,6 +552,14 @@ int qdot_b200_bound_sums(const qdot_bin* bins, int32_t n_bins, int64_t shift, do
     return QDOT_OK;
 }
 
+// two shifts in one call (the report's rel terms at e_max, then abs at 0):
+// out[0..1] for shift_a, out[2..3] for shift_b; the first failure is returned
+int qdot_b200_bound_sums2(const qdot_bin* bins, int32_t n_bins, int64_t shift_a, int64_t shift_b, double* out) {
+    if (!out) return QDOT_ERR_ARG;
+    const int r = qdot_b200_bound_sums(bins, n_bins, shift_a, out);
+    return r ? r : qdot_b200_bound_sums(bins, n_bins, shift_b, out + 2);
+}
+
 double qdot_b200_ldexp_rn(double acc, int64_t u, int* overflow) {
     int o = 0;
     double r = ldexp_rn(acc, u, &o);

@@ -14,6 +14,8 @@ from typing import Optional, Tuple
 import numpy as np
 
 from . import _lib
+from .binning import strategy_code
+from .scoring import SplitMode
 
 _tls = threading.local()
 
@@ -113,14 +115,6 @@ def stream_handle(device) -> int:
 
 
 def config_struct(cfg, strategy) -> _lib.QdotConfig:
-    from .binning import strategy_code
-    from .scoring import SplitMode
     code, param = strategy_code(strategy)
-    c = _lib.QdotConfig()
-    c.epsilon = float(cfg.epsilon)
-    c.split = 1 if cfg.split == SplitMode.PER_BIN else 0
-    c.input_mu = int(cfg.input_mu)
-    c.strategy = code
-    c.strategy_param = param
-    c.reserved = PASS1_MODE
-    return c
+    return _lib.QdotConfig(float(cfg.epsilon), 1 if cfg.split == SplitMode.PER_BIN else 0, int(cfg.input_mu), code,
+                           PASS1_MODE, param)

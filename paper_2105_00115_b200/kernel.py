@@ -197,11 +197,12 @@ assert _BIN_DTYPE.itemsize == ctypes.sizeof(_lib.QdotBin)
 
 
 def _bin_rows(cbins, n_bins: int) -> np.ndarray:
-    """A private copy of the first n_bins device bin records (the ctypes table is
-    reused by the next call on this thread)."""
+    """A private, read-only copy of the first n_bins device bin records (the
+    ctypes table is reused by the next call on this thread); string_at copies
+    the bytes without the buffer protocol's per-call format parsing."""
     if n_bins <= 0:
         return np.zeros(0, dtype=_BIN_DTYPE)
-    return np.frombuffer(cbins, dtype=_BIN_DTYPE, count=n_bins).copy()
+    return np.frombuffer(ctypes.string_at(ctypes.addressof(cbins), n_bins * _BIN_DTYPE.itemsize), dtype=_BIN_DTYPE)
 
 
 def _bound_sums(cbins, n_bins: int, shift: int):
@@ -218,6 +219,17 @@ def _bound_sums(cbins, n_bins: int, shift: int):
     return out[0], out[1]
 
 
+def _bound_sums2(cbins, n_bins: int, shift_a: int, shift_b: int):
+    """_bound_sums for two shifts in one library call: (fsum_a, plain_a, fsum_b, plain_b)."""
+    lib = _lib.load()
+    out = (ctypes.c_double * 4)()
+    rc = lib.qdot_b200_bound_sums2(cbins, int(n_bins), int(shift_a), int(shift_b), out)
+    if rc == _lib.QDOT_ERR_OVERFLOW:
+        raise OverflowError("math range error")
+    _lib.check(rc, lib)
+    return out[0], out[1], out[2], out[3]
+
+
 def _make_bin_objects(rows: np.ndarray, indexer):
     def make(ps):
         return [Bin(lower=int(r["lower"]), upper=int(r["upper"]), cardinality=int(r["cardinality"]),
@@ -227,7 +239,7 @@ def _make_bin_objects(rows: np.ndarray, indexer):
     return make
 
 
-def _build_params(res, cbins, cfg, strategy, indexer, rows=None) -> ParameterSet:
+def _build_params(res, cbins, cfg, strategy, indexer, rows=None, rel=None) -> ParameterSet:
     if rows is None:
         rows = _bin_rows(cbins, int(res.n_bins))
     ps = ParameterSet(bins=None, e_min=int(res.e_min), e_max=int(res.e_max), strategy=strategy, tolerance=cfg,
@@ -236,13 +248,23 @@ def _build_params(res, cbins, cfg, strategy, indexer, rows=None) -> ParameterSet
                       _make_bins=_make_bin_objects(rows, indexer))
     # ParameterSet.rel_bound: plain left-to-right sum from 0.0 (scoring.py:195-199);
     # the report's rel_bound: fsum of the same terms (kernel.py:213)
-    ps._rel_fsum, ps.rel_bound = _bound_sums(cbins, int(res.n_bins), int(res.e_max))
+    ps._rel_fsum, ps.rel_bound = rel if rel is not None else _bound_sums(cbins, int(res.n_bins), int(res.e_max))
     return ps
 
 
 def _prepare(x, y):
     torch = require_cuda()
     is_norm = x is y                                           # kernel.py:194
+    # fast path: 1-D contiguous float64 tensors already on the current device
+    if type(x) is torch.Tensor and (is_norm or type(y) is torch.Tensor):
+        dev = x.device
+        if (x.is_cuda and x.dtype is torch.float64 and x.dim() == 1 and x.is_contiguous()
+                and dev.index == torch.cuda.current_device()
+                and (is_norm or (y.device == dev and y.dtype is torch.float64 and y.dim() == 1
+                                 and y.is_contiguous()))):
+            if not is_norm and x.shape[0] != y.shape[0]:       # floatbits.py:68-69
+                raise ValueError(f"length mismatch: {x.shape[0]} vs {y.shape[0]}")
+            return is_norm, x, (x if is_norm else y)
     device = torch.device("cuda", torch.cuda.current_device())
     xd, _ = as_device_vector(x, device)
     yd = xd if is_norm else as_device_vector(y, device)[0]
@@ -283,8 +305,9 @@ def _raise_status(res) -> None:
 def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer) -> QdotReport:
     """Host-side report assembly (kernel.py:205-240)."""
     rows = _bin_rows(cbins, int(res.n_bins))
-    params = _build_params(res, cbins, cfg, strategy, indexer, rows)
-    abs_bound = _bound_sums(cbins, int(res.n_bins), 0)[0]
+    # the rel terms at e_max (params), then the abs terms: one library call, same order
+    rf, rp, abs_bound, _ = _bound_sums2(cbins, int(res.n_bins), int(res.e_max), 0)
+    params = _build_params(res, cbins, cfg, strategy, indexer, rows, rel=(rf, rp))
     rel_bound = params._rel_fsum
     rel_hypothesis = "assumed"
     rel_bound_e = None
