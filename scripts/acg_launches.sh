@@ -13,7 +13,7 @@ for _ in range(3):
 PY
 for mode in small four; do
   if [ $mode = small ]; then export QDOT_B200_SMALL_AUTO=65536; else export QDOT_B200_SMALL_AUTO=1; fi
-  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/acg_launch_${mode}_$TAG.csv python /tmp/acg_one.py > /dev/null 2>&1
+  timeout 300 ncu --graph-profiling node --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/acg_launch_${mode}_$TAG.csv python /tmp/acg_one.py > /dev/null 2>&1
   python - "$mode" "gpurun_out/acg_launch_${mode}_$TAG.csv" <<'PY'
 import csv, collections, sys
 rows = list(csv.reader(open(sys.argv[2])))

@@ -16,9 +16,10 @@ timeout 300 python scripts/latency.py > gpurun_out/latency_$TAG.jsonl 2>&1
 ( for n in 1000 10000 16384 32768 100000 1000000; do timeout 120 python scripts/step_graph_time.py $n; PIPE=four timeout 120 python scripts/step_graph_time.py $n; done ) > gpurun_out/step_graph_$TAG.jsonl 2>&1
 ( for n in 1000 10000 16384; do timeout 120 python scripts/small_phases.py $n; done ) > gpurun_out/small_phases_$TAG.jsonl 2>&1
 timeout 300 python scripts/acg_breakdown.py > gpurun_out/acg_breakdown_$TAG.jsonl 2>&1
-( for m in 0 32; do timeout 120 python scripts/p1_time.py --norm --mode $m; done; timeout 120 python scripts/p1_time.py ) > gpurun_out/p1_norm_$TAG.jsonl 2>&1
+( for m in 0 32; do timeout 120 python scripts/p1_time.py --norm --mode $m; done; QDOT_B200_P1_NARROW=0 timeout 120 python scripts/p1_time.py --norm; timeout 120 python scripts/p1_time.py --norm --data illcond --eps 1e-12; timeout 120 python scripts/p1_time.py ) > gpurun_out/p1_norm_$TAG.jsonl 2>&1
 timeout 300 python scripts/solver_bench.py > gpurun_out/solver_bench_$TAG.jsonl 2>&1
 timeout 600 compute-sanitizer --tool memcheck python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/memcheck_smoke_$TAG.log 2>&1
 timeout 600 compute-sanitizer --tool racecheck python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/racecheck_smoke_$TAG.log 2>&1
+timeout 600 compute-sanitizer --tool synccheck python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/synccheck_smoke_$TAG.log 2>&1
 cut -c1-300 gpurun_out/bench_$TAG.json; tail -3 gpurun_out/memcheck_smoke_$TAG.log gpurun_out/racecheck_smoke_$TAG.log
 echo done
