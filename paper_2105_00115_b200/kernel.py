@@ -302,6 +302,9 @@ def _raise_status(res) -> None:
     _lib.check(int(res.status))
 
 
+_LEVELS4 = (PrecisionLevel.PERFORATE, PrecisionLevel.HALF, PrecisionLevel.SINGLE, PrecisionLevel.DOUBLE)
+
+
 def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, indexer) -> QdotReport:
     """Host-side report assembly (kernel.py:205-240)."""
     rows = _bin_rows(cbins, int(res.n_bins))
@@ -321,10 +324,7 @@ def report_from_result(res, cbins, cfg, strategy, is_norm, reference, phase, ind
             holds = params.e_max <= fe or rows.size == 0
             rel_hypothesis = "holds" if (holds or is_norm) else "violated"
             rel_bound_e = _bound_sums(cbins, int(res.n_bins), int(fe))[0]
-    counts = {level: 0 for level in PrecisionLevel}
-    for i, level in enumerate((PrecisionLevel.PERFORATE, PrecisionLevel.HALF, PrecisionLevel.SINGLE,
-                               PrecisionLevel.DOUBLE)):
-        counts[level] = int(res.counts[i])
+    counts = dict(zip(_LEVELS4, res.counts))                  # PERFORATE, HALF, SINGLE, DOUBLE
     return QdotReport(
         value=float(res.value), counts=counts, abs_bound=abs_bound, rel_bound=rel_bound,
         abs_cap=2.0 * abs_bound, rel_guarantee=params.rel_guarantee, rel_hypothesis=rel_hypothesis,
@@ -408,9 +408,9 @@ def qdot(x, y, cfg: ToleranceConfig, strategy: Strategy = None, reference=None) 
     """
     if strategy is None:
         strategy = ExactBinning()
-    require_cuda()
+    torch = require_cuda()
     is_norm = x is y                                           # kernel.py:194
-    xh = _host_vector(x)
+    xh = None if (type(x) is torch.Tensor and x.is_cuda) else _host_vector(x)   # device tensors: no host staging
     if xh is not None and xh.shape[0] >= PIPELINE_MIN:
         yh = xh if is_norm else _host_vector(y)
         if yh is not None:
