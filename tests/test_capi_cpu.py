@@ -217,3 +217,32 @@ def test_bound_sums_match_fsum():
             continue
         assert rc == 0
         assert out[0] == f and out[1] == plain, (trial, out[0], f, out[1], plain)
+
+
+def test_bound_sums2_equals_two_calls():
+    """qdot_b200_bound_sums2 (the report's rel terms at e_max, then abs at 0, in
+    one call) returns exactly what two qdot_b200_bound_sums calls return, and the
+    first failing shift's status."""
+    import ctypes
+    import random
+
+    from paper_2105_00115_b200 import _lib
+    lib = _lib.load(build_if_missing=False)
+    rnd = random.Random(11)
+    for trial in range(800):
+        nb = rnd.randint(0, 40)
+        arr = (_lib.QdotBin * max(nb, 1))()
+        for i in range(nb):
+            b = arr[i]
+            b.cardinality = rnd.choice([1, 5, rnd.randint(1, 1 << 40)])
+            b.precision = rnd.randint(0, 3)
+            b.upper = rnd.randint(-1100, 1030) if trial % 4 == 0 else rnd.randint(-60, 60)
+        sa, sb = rnd.randint(-70, 70), rnd.choice([0, rnd.randint(-70, 70)])
+        two = (ctypes.c_double * 4)()
+        ra = lib.qdot_b200_bound_sums(arr, nb, sa, two)
+        rb = lib.qdot_b200_bound_sums(arr, nb, sb, ctypes.cast(ctypes.addressof(two) + 16, ctypes.POINTER(ctypes.c_double)))
+        one = (ctypes.c_double * 4)()
+        r = lib.qdot_b200_bound_sums2(arr, nb, sa, sb, one)
+        assert r == (ra if ra else rb)
+        if r == 0:
+            assert list(one) == list(two)
