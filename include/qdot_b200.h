@@ -154,6 +154,10 @@ int qdot_b200_enqueue(const double* x, const double* y, int64_t n, int norm, con
                       void* stream);
 int qdot_b200_small(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
                     void* stream);
+/* qdot_b200_enqueue for a workspace whose exchange regions are already zero
+ * (no begin launch on the four-launch path) */
+int qdot_b200_enqueue_zeroed(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                             void* stream);
 int64_t qdot_b200_small_max(void);   /* qdot_b200_small's limit (131072) */
 /* one-CTA scoring on the (reduced) histogram: partition, scores, precisions.
  * Replaces kernel.select_parameters' partition + scoring (kernel.py:59-72,
@@ -353,9 +357,12 @@ int qdot_b200_acg_check(const void* ws_a, const void* ws_b, const double* st, vo
  * CTA, advances st (c, beta, sqrt(c)) and does qdot_b200_acg_check's record and
  * condition.  counter = {k, cap, ticket} (device int64[3], ticket 0). */
 int qdot_b200_cg_xr(int64_t n, const void* ws_pq, double* st, double* x, const double* p, double* r,
-                    const double* q, void* stream);
+                    const double* q, void* ws_clear, void* stream);
 int qdot_b200_cg_p_check(int64_t n, const void* ws_pq, const void* ws_rr, double* st, const double* r, double* p,
-                         void* rec, long long* counter, unsigned long long handle, void* stream);
+                         void* rec, long long* counter, unsigned long long handle, void* ws_clear, void* stream);
+/* ws_clear (may be NULL): a qdot workspace whose exchange regions the kernel also
+ * zeroes (what qdot_b200_begin does) -- the loop body then runs the next qdot
+ * on it with qdot_b200_enqueue_zeroed (no begin launch) */
 /* fused power-method iteration for the loop body (apps.py:302-315): pm_div:
  * x_next = z / sqrt(c) (c = the z.z result in ws_zz; st[0] = c, st[3] = sqrt c);
  * pm_check: x = x_next, then in the last CTA lam = (x . x_next) * st[3]

@@ -81,6 +81,7 @@ SIGNATURES = {
     "qdot_b200_device_info": (_I, [ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "qdot_b200_begin": (_I, [_P, _P]),
     "qdot_b200_enqueue": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _P, _P]),
+    "qdot_b200_enqueue_zeroed": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _P, _P]),
     "qdot_b200_small": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _P, _P]),
     "qdot_b200_small_max": (_I64, []),
     "qdot_b200_pass1": (_I, [_P, _P, _I64, _I, ctypes.POINTER(QdotConfig), _I64, _P, _P]),
@@ -111,8 +112,8 @@ SIGNATURES = {
     "qdot_b200_loop_launch": (_I, [_P, _P]),
     "qdot_b200_loop_destroy": (None, [_P]),
     "qdot_b200_acg_check": (_I, [_P, _P, _P, _P, _P, ctypes.c_ulonglong, _P]),
-    "qdot_b200_cg_xr": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P]),
-    "qdot_b200_cg_p_check": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_ulonglong, _P]),
+    "qdot_b200_cg_xr": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "qdot_b200_cg_p_check": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_ulonglong, _P, _P]),
     "qdot_b200_pm_div": (_I, [_I64, _P, _P, _P, _P, _P]),
     "qdot_b200_pm_check": (_I, [_I64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_ulonglong, _P]),
     "qdot_b200_exact_workspace_bytes": (ctypes.c_size_t, []),

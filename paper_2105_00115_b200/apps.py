@@ -391,13 +391,21 @@ class _IterGraph:
         self.ws = [torch.empty(nb, dtype=torch.uint8, device=device) for _ in range(2)]
         self.st = torch.zeros(8, dtype=torch.float64, device=device)
 
-    def qdot_nodes(self, k: int, xd, yd, norm: bool, c, stream: int) -> None:
-        """The qdot pipeline into workspace k (stream-ordered, no host sync)."""
+    def qdot_nodes(self, k: int, xd, yd, norm: bool, c, stream: int, zeroed: bool = False) -> None:
+        """The qdot pipeline into workspace k (stream-ordered, no host sync);
+        zeroed: the workspace's exchange regions were cleared by an earlier node."""
         lib, ws, n = self.lib, self.ws[k].data_ptr(), int(xd.shape[0])
         xp = xd.data_ptr()
         yp = xp if norm else yd.data_ptr()
         # begin / pass 1 / score / pass 2, or the one-launch cluster path at small n
-        _lib.check(lib.qdot_b200_enqueue(xp, yp, n, int(norm), ctypes.byref(c), ws, stream), lib)
+        fn = lib.qdot_b200_enqueue_zeroed if zeroed else lib.qdot_b200_enqueue
+        _lib.check(fn(xp, yp, n, int(norm), ctypes.byref(c), ws, stream), lib)
+
+    def clear_all(self, stream: int) -> None:
+        """Zero both workspaces' exchange regions (before a loop whose body
+        clears them itself for the next iteration)."""
+        for w in self.ws:
+            _lib.check(self.lib.qdot_b200_begin(w.data_ptr(), stream), self.lib)
 
     # ---- device-resident loop: a WHILE-conditional graph whose body is one
     # iteration ending with a check kernel (qdot_b200_cg_p_check for ACG,
@@ -415,13 +423,17 @@ class _IterGraph:
                                                self.ctr.data_ptr(), handle, stream), self.lib)
 
     def cg_xr(self, x, p, r, q, stream: int) -> None:
+        """... and zero workspace 1 for the r.r qdot that follows."""
         _lib.check(self.lib.qdot_b200_cg_xr(x.shape[0], self.ws[0].data_ptr(), self.st.data_ptr(), x.data_ptr(),
-                                            p.data_ptr(), r.data_ptr(), q.data_ptr(), stream), self.lib)
+                                            p.data_ptr(), r.data_ptr(), q.data_ptr(), self.ws[1].data_ptr(), stream),
+                   self.lib)
 
     def cg_p_check(self, r, p, handle: int, stream: int) -> None:
+        """... and zero workspace 0 for the next iteration's p.Ap qdot."""
         _lib.check(self.lib.qdot_b200_cg_p_check(r.shape[0], self.ws[0].data_ptr(), self.ws[1].data_ptr(),
                                                  self.st.data_ptr(), r.data_ptr(), p.data_ptr(), self.rec.data_ptr(),
-                                                 self.ctr.data_ptr(), handle, stream), self.lib)
+                                                 self.ctr.data_ptr(), handle, self.ws[0].data_ptr(), stream),
+                   self.lib)
 
     def capture_loop(self, body):
         """Build the loop graph: `body(stream, handle)` is captured as the
@@ -548,10 +560,12 @@ def _acg(a, b, x0, tau, max_iters, cfg, strategy, torch, device, n, use_graph, e
             cst = config_struct(cfg, strategy)
 
             def body(stream, handle):
+                # the workspaces are cleared by the kernel before each qdot (cg_p_check
+                # for the next p.Ap, cg_xr for r.r): no begin launches in the loop
                 a.matvec_device(p, out=q)
-                G.qdot_nodes(0, p, q, False, cst, stream)
+                G.qdot_nodes(0, p, q, False, cst, stream, zeroed=True)
                 G.cg_xr(x, p, r, q, stream)                     # alpha = c / d; x += alpha p; r -= alpha q
-                G.qdot_nodes(1, r, r, True, cst, stream)
+                G.qdot_nodes(1, r, r, True, cst, stream, zeroed=True)
                 G.cg_p_check(r, p, handle, stream)              # beta = c_new / c; p = r + beta p; c = c_new; check
 
             a.device_arrays()                                   # host->device copies cannot be captured
@@ -560,6 +574,7 @@ def _acg(a, b, x0, tau, max_iters, cfg, strategy, torch, device, n, use_graph, e
             if entry is not None:
                 entry.G, entry.graphs, entry.bufs = G, None, (x, r, p, q)
         G.st[0] = c
+        G.clear_all(stream_handle(device))                       # workspace 0 for the first p.Ap
         while resid > tau and k < max_iters:
             rec = G.run_loop(min(max_iters - k, G.LOOP_CAP), tau)
             # the host loop's checks and trace rows, from the parsed records in bulk

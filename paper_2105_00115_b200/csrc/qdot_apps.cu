@@ -196,12 +196,25 @@ __global__ void k_acg_check(const void* ws_a, const void* ws_b, const double* st
     }
 }
 
+// zero the exchange regions (A, B, rank-local counters) of the qdot workspace
+// `ws`, grid-stride -- what qdot_b200_begin does, folded into a kernel that runs
+// anyway once the workspace's previous call has been consumed
+__device__ __forceinline__ void clear_ws(void* ws) {
+    if (!ws) return;
+    ulonglong2* z = reinterpret_cast<ulonglong2*>(static_cast<char*>(ws) + qd::OFF_A);
+    const int64_t n16 = (qd::BYTES_A + qd::BYTES_B + qd::BYTES_LOCAL) / 16;
+    for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n16; i += (int64_t)gridDim.x * T)
+        z[i] = make_ulonglong2(0ull, 0ull);
+}
+
 // ---- fused ACG iteration kernels for the device loop (apps.py:212-223):
 // x = x + alpha p and r = r - alpha q with alpha = c / d computed per thread
 // (c = st[0], d = the p.Ap dot in ws_pq); the products rounded first like the
 // numpy expressions.  Block 0 records alpha and d in st.
 __global__ void __launch_bounds__(T) k_cg_xr(int64_t n, const void* ws_pq, double* st, double* x,
-                                             const double* __restrict__ p, double* r, const double* __restrict__ q) {
+                                             const double* __restrict__ p, double* r, const double* __restrict__ q,
+                                             void* ws_clear) {
+    clear_ws(ws_clear);                          // the r.r workspace, for the qdot that follows
     const double d = result_value(ws_pq);
     const double alpha = __ddiv_rn(st[0], d);
     for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += (int64_t)gridDim.x * T) {
@@ -216,7 +229,9 @@ __global__ void __launch_bounds__(T) k_cg_xr(int64_t n, const void* ws_pq, doubl
 // advances the recurrence: st[0] = c_new, st[2] = beta, st[3] = sqrt(c_new).
 __global__ void __launch_bounds__(T) k_cg_p_check(int64_t n, const void* ws_pq, const void* ws_rr, double* st,
                                                   const double* __restrict__ r, double* p, unsigned char* rec,
-                                                  long long* counter, cudaGraphConditionalHandle handle) {
+                                                  long long* counter, cudaGraphConditionalHandle handle,
+                                                  void* ws_clear) {
+    clear_ws(ws_clear);                          // the p.Ap workspace (its result header is outside the regions)
     const double c_new = result_value(ws_rr);
     const double beta = __ddiv_rn(c_new, st[0]);
     for (int64_t i = (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += (int64_t)gridDim.x * T)
@@ -380,21 +395,21 @@ void qdot_b200_loop_destroy(void* loop) {
 }
 
 int qdot_b200_cg_xr(int64_t n, const void* ws_pq, double* st, double* x, const double* p, double* r,
-                    const double* q, void* stream) {
+                    const double* q, void* ws_clear, void* stream) {
     if (n < 0 || !ws_pq || !st || (n > 0 && (!x || !p || !r || !q))) return QDOT_ERR_ARG;
     const int g = grid_for(n > 0 ? n : 1, 4);
-    k_cg_xr<<<g, T, 0, static_cast<cudaStream_t>(stream)>>>(n, ws_pq, st, x, p, r, q);
+    k_cg_xr<<<g, T, 0, static_cast<cudaStream_t>(stream)>>>(n, ws_pq, st, x, p, r, q, ws_clear);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "cg_xr");
 }
 
 int qdot_b200_cg_p_check(int64_t n, const void* ws_pq, const void* ws_rr, double* st, const double* r, double* p,
-                         void* rec, long long* counter, unsigned long long handle, void* stream) {
+                         void* rec, long long* counter, unsigned long long handle, void* ws_clear, void* stream) {
     if (n < 0 || !ws_pq || !ws_rr || !st || !rec || !counter || (n > 0 && (!r || !p))) return QDOT_ERR_ARG;
     const int g = grid_for(n > 0 ? n : 1, 4);
     k_cg_p_check<<<g, T, 0, static_cast<cudaStream_t>(stream)>>>(n, ws_pq, ws_rr, st, r, p,
                                                                   static_cast<unsigned char*>(rec), counter,
-                                                                  (cudaGraphConditionalHandle)handle);
+                                                                  (cudaGraphConditionalHandle)handle, ws_clear);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? QDOT_OK : qd::report_cuda_error(e, "cg_p_check");
 }

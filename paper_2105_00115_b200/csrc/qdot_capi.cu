@@ -187,17 +187,27 @@ int qdot_b200_small(const double* x, const double* y, int64_t n, int norm, const
     return QDOT_OK;
 }
 
-int qdot_b200_enqueue(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
-                      void* stream) {
+static int enqueue_impl(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                        void* stream, bool begin) {
     int r;
     if (small_ok(n, cfg)) {
         if ((r = qdot_b200_small(x, y, n, norm, cfg, ws, stream))) return r;
     } else {
-        if ((r = qdot_b200_begin(ws, stream))) return r;
+        if (begin && (r = qdot_b200_begin(ws, stream))) return r;
         if ((r = qdot_b200_pass1(x, y, n, norm, cfg, n, ws, stream))) return r;
     }
     if ((r = qdot_b200_score_finalize(ws, n, cfg, stream))) return r;
     return qdot_b200_pass2_finalize(x, y, n, norm, ws, stream);
+}
+
+int qdot_b200_enqueue(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                      void* stream) {
+    return enqueue_impl(x, y, n, norm, cfg, ws, stream, true);
+}
+
+int qdot_b200_enqueue_zeroed(const double* x, const double* y, int64_t n, int norm, const qdot_config* cfg, void* ws,
+                             void* stream) {
+    return enqueue_impl(x, y, n, norm, cfg, ws, stream, false);
 }
 
 static int score_impl(void* ws, int64_t n_total, const qdot_config* cfg, bool fuse, void* stream) {
