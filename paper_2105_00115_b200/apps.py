@@ -441,7 +441,11 @@ class _IterGraph:
         torch, device = _dev()
         self.ctr = torch.zeros(3, dtype=torch.int64, device=self.st.device)    # k, cap, CTA ticket
         self.ctr_host = torch.zeros(3, dtype=torch.int64).pin_memory()
+        self.st_host = torch.zeros(8, dtype=torch.float64).pin_memory()
         self.rec = torch.empty(self.LOOP_CAP * 576, dtype=torch.uint8, device=self.st.device)
+        # read back after a launch: the counter and the first REC_HEAD records in one
+        # copy + sync, the rest only for longer runs
+        self.back = torch.empty(64 + self.REC_HEAD * 576, dtype=torch.uint8).pin_memory()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         loop = ctypes.c_void_p()
@@ -459,20 +463,37 @@ class _IterGraph:
     REC_DTYPE = np.dtype({"names": ["a", "b", "st"], "formats": [_lib.RESULT_DTYPE, _lib.RESULT_DTYPE, ("<f8", (8,))],
                           "offsets": [0, 256, 512], "itemsize": 576})
 
-    def run_loop(self, cap: int, tau: float):
-        """Run up to `cap` iterations on the device (st[0] = c set by the
-        caller); returns the recorded iterations as a numpy record array
-        (fields a / b: the two dots' result headers, st: the scalar state)."""
+    REC_HEAD = 64                                             # records read back with the counter
+
+    def run_loop(self, cap: int, tau: float, st0=None):
+        """Run up to `cap` iterations on the device; st0: {index: value} of the
+        scalar state to set first (with st[7] = tau, one host->device copy).
+        Returns the recorded iterations as a numpy record array (fields a / b:
+        the two dots' result headers, st: the scalar state)."""
         torch, _ = _dev()
         stream = torch.cuda.current_stream()
-        self.st[7] = tau
+        if st0 is not None:
+            for i, v in st0.items():
+                self.st_host[i] = v
+            self.st_host[7] = tau
+            self.st.copy_(self.st_host, non_blocking=True)
+        else:
+            self.st[7] = tau
         self.ctr_host[0] = 0
         self.ctr_host[1] = cap
         self.ctr_host[2] = 0
         self.ctr.copy_(self.ctr_host, non_blocking=True)
         _lib.check(self.lib.qdot_b200_loop_launch(self.loop, stream.cuda_stream), self.lib)
-        k = int(self.ctr[0].item())                       # waits for the loop
-        return np.frombuffer(self.rec[:k * 576].cpu().numpy().tobytes(), dtype=self.REC_DTYPE, count=k)
+        back = self.back
+        back[:24].copy_(self.ctr.view(torch.uint8), non_blocking=True)
+        back[64:].copy_(self.rec[:self.REC_HEAD * 576], non_blocking=True)
+        stream.synchronize()                                  # waits for the loop
+        k = int(back[:8].view(torch.int64)[0])
+        if k <= self.REC_HEAD:
+            raw = back[64:64 + k * 576].numpy().tobytes()
+        else:
+            raw = back[64:].numpy().tobytes() + self.rec[self.REC_HEAD * 576:k * 576].cpu().numpy().tobytes()
+        return np.frombuffer(raw, dtype=self.REC_DTYPE, count=k)
 
     def header(self, rec, field: str, i: int):
         """Record i's result header `field` as a QdotResult (error paths)."""
@@ -573,10 +594,12 @@ def _acg(a, b, x0, tau, max_iters, cfg, strategy, torch, device, n, use_graph, e
             G.capture_loop(body)
             if entry is not None:
                 entry.G, entry.graphs, entry.bufs = G, None, (x, r, p, q)
-        G.st[0] = c
         G.clear_all(stream_handle(device))                       # workspace 0 for the first p.Ap
+        first = True
         while resid > tau and k < max_iters:
-            rec = G.run_loop(min(max_iters - k, G.LOOP_CAP), tau)
+            # st[0] = c on the first launch (later chunks continue from the device's c)
+            rec = G.run_loop(min(max_iters - k, G.LOOP_CAP), tau, st0={0: c} if first else None)
+            first = False
             # the host loop's checks and trace rows, from the parsed records in bulk
             a, b = rec["a"], rec["b"]
             sa, va, ca, na = a["status"].tolist(), a["value"].tolist(), a["counts"].tolist(), a["n"].tolist()
@@ -679,9 +702,8 @@ def _apm(a, x_h, nrm, tau, max_iters, cfg, strategy, torch, device, use_graph, e
             if entry is not None:
                 entry.G, entry.graphs, entry.bufs = G, None, (x, x_next, z)
         while k < max_iters and not converged:
-            G.st[5] = 0.0 if lam_prev is None else lam_prev
-            G.st[6] = 0.0 if lam_prev is None else 1.0
-            rec = G.run_loop(min(max_iters - k, G.LOOP_CAP), tau)
+            rec = G.run_loop(min(max_iters - k, G.LOOP_CAP), tau,
+                             st0={5: 0.0 if lam_prev is None else lam_prev, 6: 0.0 if lam_prev is None else 1.0})
             ra, rb = rec["a"], rec["b"]
             sa, va, ca, na, za = (ra["status"].tolist(), ra["value"].tolist(), ra["counts"].tolist(),
                                   ra["n"].tolist(), ra["zero_count"].tolist())
